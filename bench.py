@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Benchmark of the DPD solvent step (Mirheo, arXiv:1911.04712) on B200.
+
+Metric (BASELINE.json): DPD particle-steps/s (whole job), plus the HBM-roofline fraction
+of the step (SURVEY §8d byte model) and the dominant kernel's roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config eq64] [--impl reference]
+
+N = 1 runs the BASELINE config 2 (64^3, rho = 8, 2,097,152 particles, P:483, P:489 params).
+N > 1 (under torchrun): weak scaling, one 64^3 subdomain per GPU on a 3D rank grid, NCCL.
+Prints ONE JSON line on rank 0.  See DESIGN.md §8 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "DPD particle-steps/s"
+UNIT = "particle-steps/s"
+BYTES_PER_PARTICLE_STEP = 192.0  # bin 56 + scan ~1 + scatter 88 + force 48 (rounded model)
+
+
+def rank_grid(n):
+    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(n) or _factor3(n)
+
+
+def _factor3(n):
+    best = None
+    for a in range(1, n + 1):
+        if n % a:
+            continue
+        for b in range(1, n // a + 1):
+            if (n // a) % b:
+                continue
+            c = n // a // b
+            key = max(a, b, c) - min(a, b, c)
+            if best is None or key < best[0]:
+                best = (key, (a, b, c))
+    return best[1]
+
+
+# Algorithmic work model.  Per unordered interacting pair the pair body needs
+# ~77 lane-instructions at minimum (Philox4x32-10 words: 9 rounds x (2 IMAD.WIDE + 2 LOP3)
+# + final round 2 + min/max 2 = 40; Box-Muller 9; geometry, weights, dissipative dot product,
+# magnitude and the two force updates 28); every candidate pair of the half stencil needs a
+# distance test of 7 (3 FADD, 3 FMUL/FFMA, 1 FSETP).
+INSTR_PER_PAIR = 77.0
+INSTR_PER_CANDIDATE = 7.0
+# bytes per particle and launch, SURVEY §8d byte model
+KERNEL_BYTES = {"bin": 56.0, "scatter": 88.0, "force": 48.0, "pack": 40.0, "gather": 60.0}
+
+
+def kernel_roofline(name, ms_per_launch, cfg, n_local, peaks, src):
+    sec = ms_per_launch * 1e-3
+    if name == "force":
+        vol = 4.0 * math.pi / 3.0 * cfg.rc ** 3
+        pairs = n_local * cfg.rho * vol / 2.0
+        cand = n_local * cfg.rho * 13.5 * cfg.rc ** 3
+        inst = pairs * INSTR_PER_PAIR + cand * INSTR_PER_CANDIDATE
+        clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        peak = 148 * 128 * clk / 1e12  # lane-instructions / s: 148 SMs x 4 SMSP x 32 lanes, 1 instr/cycle
+        ach = inst / sec / 1e12
+        return {"kernel": name, "bound": "alu", "achieved": ach, "peak": peak, "unit": "Tinst/s",
+                "frac": ach / peak, "traffic": None,
+                "work_model": f"{INSTR_PER_PAIR:g} instr/pair x {pairs:.4g} pairs + {INSTR_PER_CANDIDATE:g} "
+                              f"instr/candidate x {cand:.4g} candidates per launch",
+                "peak_source": "148 SM x 128 lanes x sm_max_mhz (%s)" % src,
+                "hbm_view": {"bytes_per_particle": 48.0,
+                             "achieved_gbs": 48.0 * n_local / sec / 1e9, "peak_gbs": float(peaks["hbm_gbs"])}}
+    b = KERNEL_BYTES.get(name, 0.0) * n_local
+    ach = b / sec / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+            "frac": ach / float(peaks["hbm_gbs"]), "traffic": None, "peak_source": src}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index=0, period=0.05):
+        self.samples = []
+        self.reasons = 0
+        self.period = period
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml-unavailable"]}
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference): the oracle as it stands, fp64 cell-list
+# mode (C-2 item 7) on a bounded sub-box sample of the same workload (same rho / params).
+# ------------------------------------------------------------------------------------------
+def oracle_sample_rate(cfg, target_s=15.0, sample_box=24.0, max_steps=50):
+    import oracle
+    box = tuple(min(float(b), sample_box) for b in cfg.box)
+    p = oracle.DPDParams(box=box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
+                         seed=cfg.seed, body_f=cfg.body_f)
+    pos, vel = workloads.make_particles(box, cfg.rho, cfg.kT)
+    st = oracle.State(p, pos, vel, celllist=True)
+    n = pos.shape[0]
+    t0 = time.perf_counter()
+    st.step(1)
+    dt1 = time.perf_counter() - t0
+    k = int(max(1, min(max_steps, target_s / max(dt1, 1e-6))))
+    t0 = time.perf_counter()
+    st.step(k)
+    el = time.perf_counter() - t0
+    return {"value": n * k / el, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"oracle fp64 cell-list mode, {k} steps of a {box[0]:g}x{box[1]:g}x{box[2]:g} sub-box "
+                      f"({n} particles) at the same rho={cfg.rho:g} and parameters as '{cfg.name}'"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    box = tuple(min(float(b), 24.0) for b in cfg.box)
+    p = oracle.DPDParams(box=box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
+                         seed=cfg.seed, body_f=cfg.body_f)
+    pos, vel = workloads.make_particles(box, cfg.rho, cfg.kT)
+    st = oracle.State(p, pos, vel, celllist=True)
+    n = pos.shape[0]
+    st.step(args.warmup)
+    t0 = time.perf_counter()
+    st.step(args.steps)
+    el = time.perf_counter() - t0
+    value = n * args.steps / el
+    sample = (f"oracle fp64 cell-list mode, each step a {box[0]:g}^3 sub-box ({n} particles) of '{cfg.name}' "
+              f"(same rho and parameters)")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": config_block(cfg, args, 1),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def config_block(cfg, args, world):
+    g = rank_grid(world)
+    return {"workload": f"{cfg.name}: periodic DPD box {cfg.box[0]:g}x{cfg.box[1]:g}x{cfg.box[2]:g} per GPU, "
+                        f"rho={cfg.rho:g}, a={cfg.a:g}, gamma={cfg.gamma:g}, kT={cfg.kT:g}, k={cfg.power:g}, "
+                        f"dt={cfg.dt:g}, rc={cfg.rc:g}",
+            "particles_per_gpu": cfg.n, "particles_total": cfg.n * world,
+            "rank_grid": list(g), "parallelism": f"domain-decomposition {g[0]}x{g[1]}x{g[2]}",
+            "l2": "inputs larger than L2: double-buffered state ~%.0f MB > 126 MB L2; no flush" %
+                  (cfg.n * 96 / 1e6)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="eq64")
+    ap.add_argument("--impl", default="dpd", choices=["dpd", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1911_04712_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    grid = rank_grid(world)
+    gbox = tuple(cfg.box[k] * grid[k] for k in range(3))
+    stream = torch.cuda.Stream()
+
+    # --- build the context and the workload -------------------------------------------------
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (np.zeros(128, np.uint8))
+            code = capi.load().dpd_nccl_unique_id(capi._ptr(buf))
+            if code != 0:
+                raise RuntimeError("dpd_nccl_unique_id failed")
+            uid = torch.from_numpy(buf)
+        uid = uid.cuda()
+        dist.broadcast(uid, 0)
+        uidh = uid.cpu().numpy().astype(np.uint8)
+        ctx = capi.dpd_create_dist(gbox, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed, rank, world,
+                                   grid, uidh)
+    else:
+        ctx = capi.dpd_create(gbox, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
+    capi.dpd_set_stream(ctx, stream.cuda_stream)
+    if cfg.body_f:
+        capi.dpd_set_body_force(ctx, cfg.body_f)
+    # each rank generates only its own subdomain's particles with globally unique ids
+    coord = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
+    pos, vel = workloads.make_particles(cfg.box, cfg.rho, cfg.kT, init_seed=1 + rank)
+    pos = (pos + np.array([coord[k] * cfg.box[k] for k in range(3)], np.float32)).astype(np.float32)
+    n_local = pos.shape[0]
+    ids = (np.arange(n_local, dtype=np.int64) + rank * n_local).astype(np.int32)
+    pos_h = torch.from_numpy(pos).pin_memory()
+    vel_h = torch.from_numpy(vel).pin_memory()
+    ids_h = torch.from_numpy(ids).pin_memory()
+    capi.dpd_set_particles_ex(ctx, pos_h, vel_h, ids_h if world > 1 else None, 0)
+    n_total = n_local * world
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # --- warm-up -----------------------------------------------------------------------
+    capi.dpd_step(ctx, args.warmup)
+
+    # --- timed region: K steps, inputs resident in HBM ----------------------------------
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = capi.dpd_get_launch_count(ctx)
+    barrier()
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(stream)
+        capi.dpd_step_async(ctx, args.steps)
+        ev1.record(stream)
+        capi.dpd_sync(ctx)
+    barrier()
+    launches = capi.dpd_get_launch_count(ctx) - l0
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = n_total * args.steps / (ms * 1e-3)
+
+    # --- per-kernel times (CUDA events around each launch, same stream), K steps ----------
+    capi.dpd_set_timing(ctx, True)
+    capi.dpd_step(ctx, args.steps)
+    ktimes = capi.dpd_get_timing(ctx)
+    capi.dpd_set_timing(ctx, False)
+    per_kernel = {k: {"ms_per_launch": v[0] / max(v[1], 1), "launches": v[1]} for k, v in ktimes.items() if v[1]}
+    step_kernel_ms = sum(v[0] for k, v in ktimes.items()) / args.steps
+
+    # --- e2e: public API with host buffers (set -> step(K) -> get), copies inside ---------
+    e2e = None
+    if not args.no_e2e:
+        out_pos = torch.empty((n_local, 3), dtype=torch.float32).pin_memory()
+        out_vel = torch.empty((n_local, 3), dtype=torch.float32).pin_memory()
+        out_ids = torch.empty((n_local * 2 + 1024,), dtype=torch.int32).pin_memory()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        capi.dpd_set_particles_ex(ctx, pos_h, vel_h, ids_h if world > 1 else None, 0)
+        capi.dpd_step_async(ctx, args.steps)
+        if world > 1:
+            big_p = torch.empty((n_local * 2 + 1024, 3), dtype=torch.float32).pin_memory()
+            big_v = torch.empty((n_local * 2 + 1024, 3), dtype=torch.float32).pin_memory()
+            capi.dpd_get_particles_ex(ctx, big_p, big_v, out_ids)
+        else:
+            capi.dpd_get_particles(ctx, out_pos, out_vel)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ems = float(te.item())
+        h2d = n_local * (24 + (4 if world > 1 else 0))
+        d2h = n_local * 24
+        e2e = {"value": n_total * args.steps / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d * world / args.steps, "d2h_bytes_per_step": d2h * world / args.steps,
+               "note": "set_particles(pinned host) + dpd_step(K) + get_particles(pinned host); "
+                       "bytes amortised over the K steps of one call sequence"}
+
+    # --- roofline --------------------------------------------------------------------------
+    peaks, peaks_src = measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    step_bytes_gbs = BYTES_PER_PARTICLE_STEP * (n_total / world) / (ms_per_step * 1e-3) / 1e9
+    dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms_per_launch"] * kv[1]["launches"])[0] if per_kernel else None
+    roof = None
+    if dom:
+        roof = kernel_roofline(dom, per_kernel[dom]["ms_per_launch"], cfg, n_local, peaks, peaks_src)
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic: uniform positions, Maxwell-Boltzmann velocities",
+           "config": config_block(cfg, args, world), "clocks": clocks.summary(), "gpu_launches": launches,
+           "roofline": roof,
+           "step_roofline": {"bound": "hbm", "bytes_per_particle_step": BYTES_PER_PARTICLE_STEP,
+                             "achieved": step_bytes_gbs, "peak": hbm, "unit": "GB/s",
+                             "frac": step_bytes_gbs / hbm, "peak_source": peaks_src},
+           "kernels": per_kernel, "kernel_ms_per_step": step_kernel_ms, "e2e": e2e}
+
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = oracle_sample_rate(cfg)
+        except Exception as exc:  # noqa: BLE001
+            out["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    capi.dpd_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,193 @@
+/*
+ * dpd.h -- C-ABI of the B200-native DPD solvent step (Mirheo, arXiv:1911.04712).
+ *
+ * One library (libdpd.so, sources in paper_1911_04712_b200/csrc/) owns all device state.
+ * Every entry point is extern "C", takes plain pointers and sizes, and returns one of the
+ * DPD_* status codes below (never throws, never aborts).  On failure the context keeps a
+ * message readable with dpd_last_error().  A context is NOT thread-safe: calls on one
+ * context must be serialised by the caller.
+ *
+ * Citation convention: P:n = PAPER.md line n (section named), C-n = reading adopted in
+ * DESIGN.md §3.  The method:
+ *   - particles evolve by Newton's law dr/dt = v, dv/dt = F/m, m = 1      (C-18)
+ *   - F_i = sum_j (F^C + F^D + F^R) over j within r_c                     (eq. 2)
+ *     F^C = a w e, w = 1 - r/r_c;  F^D = -gamma w_D (v_ij.e) e;
+ *     F^R = sigma xi_ij w_R e / sqrt(dt);  w_R = w^k, w_D = w_R^2,
+ *     sigma^2 = 2 gamma kT                                               (C-3, C-4)
+ *   - xi_ij from Philox4x32-10(ctr = {min id, max id, step lo, step hi},
+ *     key = {seed lo, seed hi}), Box-Muller on words 0,1                  (C-7)
+ *   - cell lists of edge >= r_c rebuilt every step
+ *   - "fused Velocity-Verlet" = Groot-Warren VV, lambda = 1/2             (C-6)
+ *   - 3D domain decomposition with ghost exchange and redistribution
+ *
+ * Host-side layouts: positions / velocities / forces are n x 3 row-major float32 (AoS
+ * xyz).  Pointers passed to set/get may be host (pageable or pinned) or device memory
+ * (copies use cudaMemcpyDefault under unified addressing).  Positions outside [0, L) are
+ * wrapped on input (C-10).
+ */
+#ifndef DPD_H
+#define DPD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dpd_ctx dpd_ctx; /* opaque; owns all device memory of one (sub)domain */
+
+enum {
+    DPD_OK = 0,
+    DPD_ERR_ARG = 1,      /* bad argument (null pointer, n mismatch, ids not dense, ...)   */
+    DPD_ERR_CONFIG = 2,   /* invalid parameters: rc<=0, box < 3 rc, power not in (0,1] ... */
+    DPD_ERR_CUDA = 3,     /* CUDA runtime error (message in dpd_last_error)               */
+    DPD_ERR_NUMERIC = 4,  /* non-finite position/velocity/force (input or during a step)  */
+    DPD_ERR_CAPACITY = 5, /* a device buffer (cell, ghost, migration) overflowed          */
+    DPD_ERR_COMM = 6      /* NCCL error (multi-GPU)                                       */
+};
+
+/* Create a single-GPU context on the current CUDA device for a periodic box.
+ *   box[3]  : box edge lengths L_x, L_y, L_z (> 0; each >= 3 rc so the 27-cell stencil
+ *             has distinct cells)
+ *   rc      : cutoff radius (> 0)
+ *   a       : conservative amplitude (>= 0)
+ *   gamma   : dissipative coefficient (>= 0)
+ *   kT      : temperature (>= 0); sigma = sqrt(2 gamma kT) is derived
+ *   power   : kernel exponent k in (0, 1]; w_R = w^k                          P:136, C-4
+ *   dt      : time step (> 0)
+ *   seed    : 64-bit Philox key of the pair RNG                               C-7
+ *   out     : receives the new context (NULL on failure)
+ * Returns DPD_OK, DPD_ERR_ARG (out == NULL), DPD_ERR_CONFIG or DPD_ERR_CUDA. */
+int dpd_create(const double box[3], double rc, double a, double gamma, double kT,
+               double power, double dt, uint64_t seed, dpd_ctx **out);
+
+/* Destroy a context and free its device memory.  NULL is a no-op. */
+void dpd_destroy(dpd_ctx *ctx);
+
+/* Message for the last failed call on ctx ("" if none).  Owned by ctx. */
+const char *dpd_last_error(const dpd_ctx *ctx);
+
+/* Launch all work on this CUDA stream (a cudaStream_t; NULL = the context's own
+ * non-blocking stream, the default).  The caller keeps ownership of the stream. */
+int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
+
+/* Periodic-Poiseuille body force: f_body = (0,0,-f) for r_x <= L_x/2 and
+ * (0,0,+f) otherwise (global coordinates).  f = 0 (default) disables it.  The body force
+ * enters the integrator, not dpd_get_forces. */
+int dpd_set_body_force(dpd_ctx *ctx, double f);
+
+/* Load n particles (copied; the caller keeps its buffers), assign ids 0..n-1, set the
+ * step counter s = 0, build the cell list and prime F_0 = F(x_0, v_0, s=0) (C-2 item 2).
+ *   pos, vel : n x 3 float32; pos is wrapped into [0, L) (C-10)
+ * n = 0 is legal.  Non-finite input -> DPD_ERR_NUMERIC. */
+int dpd_set_particles(dpd_ctx *ctx, int64_t n, const float *pos, const float *vel);
+
+/* As dpd_set_particles, with caller-chosen global ids (each < 2^31, unique) and the
+ * starting step index step0 (checkpoint resume, C-20).  In a distributed context every
+ * rank may pass any superset of its particles: each rank keeps those inside its
+ * subdomain.  ids may be NULL (ids := 0..n-1). */
+int dpd_set_particles_ex(dpd_ctx *ctx, int64_t n, const float *pos, const float *vel,
+                         const int32_t *ids, int64_t step0);
+
+/* Advance nsteps >= 0 steps of Groot-Warren VV (C-2 item 3):
+ *   u = v + dt/2 (F + f_body);  x = wrap(x + dt u);  s += 1;  rebuild cells;
+ *   F = F(x, u, s);  v = u + dt/2 (F + f_body)
+ * implemented fused (kick-drift on the half-step velocity u).
+ * Synchronises the context's stream before returning and reports the first device-side
+ * error (DPD_ERR_NUMERIC / DPD_ERR_CAPACITY / DPD_ERR_COMM). */
+int dpd_step(dpd_ctx *ctx, int64_t nsteps);
+
+/* As dpd_step but does not synchronise; a device-side error is reported by the next
+ * synchronising call (dpd_step, dpd_get_*, dpd_sync). */
+int dpd_step_async(dpd_ctx *ctx, int64_t nsteps);
+
+/* Wait for the context's stream and report any pending device-side error. */
+int dpd_sync(dpd_ctx *ctx);
+
+/* Number of particles currently owned by this context (local particles when distributed). */
+int dpd_get_count(const dpd_ctx *ctx, int64_t *n);
+
+/* Step counter s (completed steps since set_particles, plus step0). */
+int dpd_get_step(const dpd_ctx *ctx, int64_t *step);
+
+/* Positions x_s and FULL-STEP velocities v_s = u_s + dt/2 (F_s + f_body) (C-6, C-14),
+ * written in id order: row id of pos/vel.  Requires the owned ids to be exactly 0..n-1
+ * (true after dpd_set_particles on one GPU), else DPD_ERR_ARG.  n must equal the count. */
+int dpd_get_particles(dpd_ctx *ctx, int64_t n, float *pos, float *vel);
+
+/* DPD pair forces F_s = F(x_s, u_s, s) (body force excluded), id order as above. */
+int dpd_get_forces(dpd_ctx *ctx, int64_t n, float *f);
+
+/* Raw state in storage (cell-sorted) order: x_s, the half-step velocity u_s used for F_s
+ * (v_0 right after set_particles), F_s and ids.  Any pointer may be NULL.  cap is the
+ * row capacity of the buffers; *n receives the count (DPD_ERR_ARG if cap < count). */
+int dpd_get_state(dpd_ctx *ctx, int64_t cap, float *pos, float *uhalf, float *f,
+                  int32_t *ids, int64_t *n);
+
+/* Cell list of the current positions (C-8): cell_of_id[id] (ids must be dense 0..n-1; may
+ * be NULL), count[ncell] and start[ncell + 1] (exclusive scan; may be NULL).  ncell is the
+ * product of dpd_get_grid's dims.  Single-GPU contexts only. */
+int dpd_debug_cells(dpd_ctx *ctx, int32_t *cell_of_id, int32_t *count, int32_t *start);
+
+/* Grid dims n_d = floor(L_d / rc) (C-8) of this context's (sub)domain. */
+int dpd_get_grid(const dpd_ctx *ctx, int32_t dims[3]);
+
+/* Re-run the force pass on the current state in recording mode and dump every interacting
+ * pair as (min id, max id, w0, w1) (T3 parity).  quad: cap x 4 uint32; *npairs receives the
+ * total (may exceed cap; only cap rows are written).  Forces are recomputed identically. */
+int dpd_debug_pairs(dpd_ctx *ctx, int64_t cap, uint32_t *quad, int64_t *npairs);
+
+/* Per-kernel timing with CUDA events on the launch stream (disables CUDA-graph replay
+ * while on).  Kernel ids: see dpd_kernel_name.  total_ms: summed event time since the
+ * last reset; launches: number of timed launches. */
+int dpd_set_timing(dpd_ctx *ctx, int enable);
+int dpd_get_timing(dpd_ctx *ctx, int kernel_id, double *total_ms, int64_t *launches);
+const char *dpd_kernel_name(int kernel_id); /* NULL past the last id */
+
+/* Number of kernel launches issued by this context since creation (all kinds). */
+int dpd_get_launch_count(const dpd_ctx *ctx, int64_t *launches);
+
+/* ---- multi-GPU (3D domain decomposition) ---------------------------------- */
+
+/* Write a fresh NCCL unique id (128 bytes) for rank 0 to broadcast to the others. */
+int dpd_nccl_unique_id(uint8_t id[128]);
+
+/* Create the context of one rank of a world of size prod(grid) over NCCL.
+ * box/rc/.../seed as dpd_create (the GLOBAL box); rank in [0, world);
+ * grid[3] = ranks per dimension (rank = gx + grid_x (gy + grid_y gz));
+ * nccl_id = the 128-byte id from dpd_nccl_unique_id on rank 0.
+ * Each subdomain must be >= 3 rc wide in every dimension. */
+int dpd_create_dist(const double box[3], double rc, double a, double gamma, double kT,
+                    double power, double dt, uint64_t seed, int rank, int world,
+                    const int32_t grid[3], const uint8_t nccl_id[128], dpd_ctx **out);
+
+/* Create an in-process group of prod(grid) subdomain contexts on the current device that
+ * exchange ghosts / migrants by device copies instead of NCCL (same kernels, transport
+ * swapped; used to test the decomposition on one GPU).  out receives grid-many contexts
+ * in rank order.  Step them together with dpd_group_step. */
+int dpd_create_group(const double box[3], double rc, double a, double gamma, double kT,
+                     double power, double dt, uint64_t seed, const int32_t grid[3],
+                     dpd_ctx **out);
+int dpd_group_step(dpd_ctx **ctxs, int nctx, int64_t nsteps);
+
+/* Local particles of a distributed context in storage order, with global ids, positions
+ * in GLOBAL coordinates and full-step velocities.  *n receives the local count. */
+int dpd_get_particles_ex(dpd_ctx *ctx, int64_t cap, float *pos, float *vel, int32_t *ids,
+                         int64_t *n);
+
+/* Forces of the local particles in storage order (same order as dpd_get_particles_ex). */
+int dpd_get_forces_ex(dpd_ctx *ctx, int64_t cap, float *f, int32_t *ids, int64_t *n);
+
+/* ---- debug / parity hooks (T0: device RNG against the Random123 known answers) ------- */
+
+/* Run the device Philox4x32-10 on n counters: ctr n x 4, key n x 2, out n x 4 (uint32). */
+int dpd_debug_philox(int64_t n, const uint32_t *ctr, const uint32_t *key, uint32_t *out);
+
+/* Device pair words and Box-Muller xi for n (ida, idb, step lo, step hi) quads under seed:
+ * words n x 2 (w0, w1), xi n floats.  Host pointers. */
+int dpd_debug_pair_words(int64_t n, const uint32_t *quad_in, uint64_t seed, uint32_t *words, float *xi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPD_H */

@@ -76,7 +76,8 @@ def lib():
         L.oracle_pair_force.restype = C.c_int
         L.oracle_min_image.argtypes = [P(Params), dp, dp, dp]
         L.oracle_forces.argtypes = [P(Params), i64, dp, dp, P(u32), i64, d, dp, dp, P(i64)]
-        L.oracle_pairs.argtypes = [P(Params), i64, dp, P(u32), i64, d, i64, P(u32), P(C.c_uint8)]
+        L.oracle_forces_subset.argtypes = [P(Params), i64, dp, dp, P(u32), i64, d, i64, P(i64), dp, dp]
+        L.oracle_pairs.argtypes =[P(Params), i64, dp, P(u32), i64, d, i64, P(u32), P(C.c_uint8)]
         L.oracle_pairs.restype = i64
         L.oracle_grid_dims.argtypes = [P(Params), P(C.c_int32)]
         L.oracle_cells.argtypes = [P(Params), i64, P(C.c_float), P(C.c_int32), P(C.c_int32), P(C.c_int32)]
@@ -167,6 +168,22 @@ def forces(p: DPDParams, x, v, step: int, ids=None, eps: float = 0.0):
                         int(step), float(eps), _p(F, C.c_double), _p(allow, C.c_double),
                         C.byref(npairs))
     return F, allow, int(npairs.value)
+
+
+def forces_subset(p: DPDParams, x, v, step: int, sel, ids=None, eps: float = 0.0):
+    """PairForces for the selected particles only (same all-j sum).  Returns (F[m,3], allow[m])."""
+    x, v = _f64(x), _f64(v)
+    n = x.shape[0]
+    ids = _ids(n, ids)
+    sel = np.ascontiguousarray(sel, dtype=np.int64)
+    m = sel.shape[0]
+    F = np.zeros((m, 3))
+    allow = np.zeros(m)
+    pc = p.c()
+    lib().oracle_forces_subset(C.byref(pc), n, _p(x, C.c_double), _p(v, C.c_double), _p(ids, C.c_uint32),
+                               int(step), float(eps), m, _p(sel, C.c_int64), _p(F, C.c_double),
+                               _p(allow, C.c_double))
+    return F, allow
 
 
 def forces_celllist(p: DPDParams, x, v, step: int, ids=None):

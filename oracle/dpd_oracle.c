@@ -200,6 +200,45 @@ int oracle_forces(const oracle_params *p, int64_t n, const double *x, const doub
     return 0;
 }
 
+/* PairForces restricted to the particles listed in sel[0..m): the same all-j sum as
+ * oracle_forces for each selected i (sampled parity at full size, where the O(N^2) sweep
+ * over every i is out of reach).  F and allow are m x 3 / m. */
+int oracle_forces_subset(const oracle_params *p, int64_t n, const double *x, const double *v,
+                         const uint32_t *ids, int64_t step, double eps, int64_t m, const int64_t *sel,
+                         double *F, double *allow)
+{
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t k = 0; k < m; ++k) {
+        const int64_t i = sel[k];
+        double Fi[3] = {0.0, 0.0, 0.0};
+        double al = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double d[3], vij[3], f[3], xi = 0.0;
+            oracle_min_image(p, &x[3 * i], &x[3 * j], d);
+            double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+            if (r2 >= (p->rc + eps) * (p->rc + eps)) continue; /* no force, not a boundary pair */
+            for (int c = 0; c < 3; ++c) vij[c] = v[3 * i + c] - v[3 * j + c];
+            int hit = oracle_pair_force(p, d, vij, ids[i], ids[j], step, f, &xi);
+            if (hit) { Fi[0] += f[0]; Fi[1] += f[1]; Fi[2] += f[2]; }
+            double r = sqrt(r2);
+            if (fabs(r - p->rc) < eps) {
+                if (!hit) {
+                    uint32_t wds[2];
+                    oracle_pair_words(p->seed, step, ids[i], ids[j], wds);
+                    xi = oracle_xi(wds[0], wds[1]);
+                }
+                al += boundary_bound(p, eps, vij, xi);
+            }
+        }
+        F[3 * k + 0] = Fi[0];
+        F[3 * k + 1] = Fi[1];
+        F[3 * k + 2] = Fi[2];
+        allow[k] = al;
+    }
+    return 0;
+}
+
 /* Enumerate unordered pairs (brute force), for pair-set / RNG-word parity (T3).
  * Every pair i<j that interacts (0 < r^2 < r_c^2) or lies within eps of the cutoff
  * (|r - r_c| < eps, a boundary pair, C-12) is written as (min id, max id, w0, w1) into

@@ -1,0 +1,434 @@
+// dpd_kernels.cuh -- the kernels of one DPD time step on sm_100a (single-GPU path).
+//
+// Step, all on one stream:
+//   k_bin      a1+a2  kick-drift-wrap in registers, cell index, warp-aggregated atomic
+//                     histogram -> rank within cell
+//   k_scan     a3     single-pass exclusive scan of the counts (decoupled look-back)
+//   k_scatter  a4     recompute a1 bit-identically, write the cell-sorted copy
+//   k_force    a5     half-stencil pair sweep, Newton-3 via atomics
+//   (a6, the second half-kick, is folded into the next step's kick and into the getters)
+#pragma once
+
+#include "dpd_device.cuh"
+
+namespace dpd {
+
+// Error word bits (device int err[4]: [0] flags, [1] offending id, [2] overflow amount)
+enum : int { ERR_NONFINITE = 1, ERR_CAPACITY = 2, ERR_RANGE = 4 };
+
+__device__ __forceinline__ void raise_err(int *err, int bit, int id)
+{
+    if ((atomicOr(&err[0], bit) & bit) == 0) err[1] = id;
+}
+
+__device__ __forceinline__ bool finite3(float a, float b, float c)
+{
+    return isfinite(a) && isfinite(b) && isfinite(c);
+}
+
+// Wrap into [0, L) (C-10): x<0 -> x+L; x>=L -> x-L; then x>=L -> 0.
+__device__ __forceinline__ float wrap_coord(float x, float L)
+{
+    if (x < 0.0f) x = __fadd_rn(x, L);
+    else if (x >= L) x = __fsub_rn(x, L);
+    if (x >= L) x = 0.0f;
+    return x;
+}
+
+// Linear index of the cell holding local position (x, y, z) (C-8), extended grid.
+__device__ __forceinline__ int cell_index(const Geom &g, float x, float y, float z)
+{
+    const int ix = cell_coord(x, g.inv_h[0], g.n[0]) + g.off[0];
+    const int iy = cell_coord(y, g.inv_h[1], g.n[1]) + g.off[1];
+    const int iz = cell_coord(z, g.inv_h[2], g.n[2]) + g.off[2];
+    return ix + g.ext[0] * (iy + g.ext[1] * iz);
+}
+
+// First half of GW-VV fused with the previous step's second half (C-6):
+//   u' = u + kick (F + f_body(x));  x' = wrap(x + dt u')
+// Explicit _rn intrinsics pin the rounding so k_bin and k_scatter agree bit-for-bit.
+__device__ __forceinline__ void advance(const Geom &g, const IntegP &ip, const float4 p, const float4 v,
+                                        const float4 f, float3 &xn, float3 &un)
+{
+    const float fb = (p.x <= ip.x_half) ? -ip.body_f : ip.body_f;
+    un.x = __fmaf_rn(ip.kick, f.x, v.x);
+    un.y = __fmaf_rn(ip.kick, f.y, v.y);
+    un.z = __fmaf_rn(ip.kick, __fadd_rn(f.z, fb), v.z);
+    xn.x = __fmaf_rn(ip.dt, un.x, p.x);
+    xn.y = __fmaf_rn(ip.dt, un.y, p.y);
+    xn.z = __fmaf_rn(ip.dt, un.z, p.z);
+    if (!g.split[0]) xn.x = wrap_coord(xn.x, g.L[0]);
+    if (!g.split[1]) xn.y = wrap_coord(xn.y, g.L[1]);
+    if (!g.split[2]) xn.z = wrap_coord(xn.z, g.L[2]);
+}
+
+__device__ __forceinline__ bool in_local_box(const Geom &g, const float3 &x)
+{
+    return x.x >= 0.0f && x.x < g.L[0] && x.y >= 0.0f && x.y < g.L[1] && x.z >= 0.0f && x.z < g.L[2];
+}
+
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Warp-aggregated atomic histogram: returns this lane's rank within cell c (c < 0: none).
+__device__ __forceinline__ int warp_rank_in_cell(int *count, int c)
+{
+    const unsigned mask = __match_any_sync(0xffffffffu, c);
+    const int leader = __ffs(mask) - 1;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == leader && c >= 0) base = atomicAdd(&count[c], __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return base + __popc(mask & lanemask_lt());
+}
+
+// ---------------------------------------------------------------------------------------
+// Input packing (set_particles): AoS xyz -> pos4 (x, y, z, id bits), vel4; wrap (C-10).
+// ---------------------------------------------------------------------------------------
+__global__ void k_pack_input(const float *__restrict__ pos3, const float *__restrict__ vel3,
+                             const int32_t *__restrict__ ids, int64_t n, Geom g, float4 *__restrict__ pos4,
+                             float4 *__restrict__ vel4, float4 *__restrict__ frc4, int *err)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float x = pos3[3 * i + 0], y = pos3[3 * i + 1], z = pos3[3 * i + 2];
+    const float vx = vel3[3 * i + 0], vy = vel3[3 * i + 1], vz = vel3[3 * i + 2];
+    const int id = ids ? ids[i] : (int)i;
+    if (!finite3(x, y, z) || !finite3(vx, vy, vz)) {
+        raise_err(err, ERR_NONFINITE, id);
+        x = y = z = 0.0f;
+    }
+    // periodic wrap by whole multiples of L (input may lie several boxes away)
+    x = wrap_coord(x - g.L[0] * floorf(x / g.L[0]), g.L[0]);
+    y = wrap_coord(y - g.L[1] * floorf(y / g.L[1]), g.L[1]);
+    z = wrap_coord(z - g.L[2] * floorf(z / g.L[2]), g.L[2]);
+    pos4[i] = make_float4(x, y, z, __int_as_float(id));
+    vel4[i] = make_float4(vx, vy, vz, 0.0f);
+    frc4[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+}
+
+// ---------------------------------------------------------------------------------------
+// a1 + a2: kick, drift, wrap, cell index, atomic histogram.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bin(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                                             const float4 *__restrict__ frc, int n, Geom g, IntegP ip,
+                                             int *__restrict__ count, int *__restrict__ rank, int *err)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int c = -1;
+    if (i < n) {
+        const float4 p = pos[i], v = vel[i], f = frc[i];
+        float3 xn, un;
+        advance(g, ip, p, v, f, xn, un);
+        if (!finite3(xn.x, xn.y, xn.z) || !finite3(un.x, un.y, un.z) || !in_local_box(g, xn)) {
+            raise_err(err, finite3(un.x, un.y, un.z) ? ERR_RANGE : ERR_NONFINITE, __float_as_int(p.w));
+            xn = make_float3(0.0f, 0.0f, 0.0f);
+        }
+        c = cell_index(g, xn.x, xn.y, xn.z);
+    }
+    const int r = warp_rank_in_cell(count, c);
+    if (i < n) rank[i] = r;
+}
+
+// ---------------------------------------------------------------------------------------
+// a3: exclusive scan start[c] = sum_{c'<c} count[c'], start[ncell] = total; count := 0
+// for the next step.  Single pass, decoupled look-back over 4096-cell tiles; the tile
+// status words carry a launch epoch kept on the device (graph-replay safe).
+// ---------------------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ unsigned long long scan_pack(unsigned epoch, int flag, int value)
+{
+    return ((unsigned long long)((epoch << 2) | (unsigned)flag) << 32) | (unsigned)value;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, int *__restrict__ start,
+                                                       int ncell, unsigned long long *tstate,
+                                                       unsigned *epoch_ptr)
+{
+    __shared__ int warp_sums[kScanThreads / 32];
+    __shared__ int tile_prefix;
+    __shared__ unsigned s_epoch;
+    const int tile = blockIdx.x;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) s_epoch = *((volatile unsigned *)epoch_ptr) + 1u;
+    const int base = tile * kScanTile + t * kScanItems;
+    int v[kScanItems];
+    if (base + kScanItems <= ncell) {
+        const int4 *src = reinterpret_cast<const int4 *>(count + base);
+#pragma unroll
+        for (int q = 0; q < kScanItems / 4; ++q) {
+            const int4 a = src[q];
+            v[4 * q + 0] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = (base + k < ncell) ? count[base + k] : 0;
+    }
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) sum += v[k];
+    // block exclusive scan of the per-thread sums
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    const unsigned epoch = s_epoch;
+    int warp_off = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+        const int s = warp_sums[w];
+        if (w < warp) warp_off += s;
+        total += s;
+    }
+    int excl = warp_off + incl - sum;
+    // publish and look back
+    if (warp == 0) {
+        volatile unsigned long long *vs = tstate;
+        if (tile == 0) {
+            if (lane == 0) {
+                vs[0] = scan_pack(epoch, 2, total);
+                tile_prefix = 0;
+            }
+        } else {
+            if (lane == 0) vs[tile] = scan_pack(epoch, 1, total);
+            int prefix = 0;
+            int pred = tile - 1;
+            while (true) {
+                const int idx = pred - lane;
+                unsigned long long st = idx >= 0 ? vs[idx] : scan_pack(epoch, 2, 0);
+                unsigned hi = (unsigned)(st >> 32);
+                int flag = ((hi >> 2) == epoch) ? (int)(hi & 3u) : 0;
+                if (__any_sync(0xffffffffu, flag == 0)) continue; // a predecessor not yet published
+                const unsigned incl_mask = __ballot_sync(0xffffffffu, flag == 2);
+                const int val = (int)(unsigned)st;
+                if (incl_mask) {
+                    const int first = __ffs(incl_mask) - 1; // nearest inclusive predecessor
+                    int s = lane <= first ? val : 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    prefix += s;
+                    break;
+                }
+                int s = val;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                prefix += s;
+                pred -= 32;
+            }
+            if (lane == 0) {
+                vs[tile] = scan_pack(epoch, 2, prefix + total);
+                tile_prefix = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    excl += tile_prefix;
+    if (base + kScanItems <= ncell) {
+        int4 *dst = reinterpret_cast<int4 *>(start + base);
+        int4 *cz = reinterpret_cast<int4 *>(count + base);
+#pragma unroll
+        for (int q = 0; q < kScanItems / 4; ++q) {
+            int4 o;
+            o.x = excl; excl += v[4 * q + 0];
+            o.y = excl; excl += v[4 * q + 1];
+            o.z = excl; excl += v[4 * q + 2];
+            o.w = excl; excl += v[4 * q + 3];
+            dst[q] = o;
+            cz[q] = make_int4(0, 0, 0, 0);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (base + k < ncell) {
+                start[base + k] = excl;
+                count[base + k] = 0;
+            }
+            excl += v[k];
+        }
+    }
+    if (tile == gridDim.x - 1) {
+        if (t == kScanThreads - 1) start[ncell] = tile_prefix + total;
+        if (t == 0) *((volatile unsigned *)epoch_ptr) = epoch; // every tile has read it by now
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// a4: scatter into cell order; recomputes a1 in registers (bit-identical to k_bin).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                                                 const float4 *__restrict__ frc, int n, Geom g, IntegP ip,
+                                                 const int *__restrict__ start, const int *__restrict__ rank,
+                                                 float4 *__restrict__ pos_o, float4 *__restrict__ vel_o,
+                                                 float4 *__restrict__ frc_o)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = pos[i], v = vel[i], f = frc[i];
+    float3 xn, un;
+    advance(g, ip, p, v, f, xn, un);
+    if (!finite3(xn.x, xn.y, xn.z) || !finite3(un.x, un.y, un.z) || !in_local_box(g, xn))
+        xn = make_float3(0.0f, 0.0f, 0.0f);
+    const int c = cell_index(g, xn.x, xn.y, xn.z);
+    const int dst = start[c] + rank[i];
+    pos_o[dst] = make_float4(xn.x, xn.y, xn.z, p.w);
+    vel_o[dst] = make_float4(un.x, un.y, un.z, 0.0f);
+    frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+}
+
+// ---------------------------------------------------------------------------------------
+// a5 (reference kernel, v1): one thread per particle i of the sorted arrays; j over the
+// own cell (j > i) and the 13 forward neighbour cells; F_i in registers, F_j -= f via
+// vector atomics.  RECORD dumps (lo id, hi id, w0, w1) of every pair.
+// ---------------------------------------------------------------------------------------
+struct PairRec {
+    uint4 *quad;
+    unsigned long long *count;
+    long long cap;
+};
+
+__constant__ int c_fwd[14][3] = {{0, 0, 0},  {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},  {1, 1, 0},
+                                 {-1, -1, 1}, {0, -1, 1}, {1, -1, 1}, {-1, 0, 1}, {0, 0, 1},
+                                 {1, 0, 1},  {-1, 1, 1}, {0, 1, 1},  {1, 1, 1}};
+
+__device__ __forceinline__ void atomic_add_f3(float4 *p, float x, float y, float z)
+{
+    atomicAdd(p, make_float4(x, y, z, 0.0f));
+}
+
+template <bool RECORD, int KMODE>
+__global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                                                   float4 *frc, const int *__restrict__ start, int n, Geom g,
+                                                   PairP pp, uint32_t s_lo, uint32_t s_hi, PairRec rec)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 pi = pos[i], vi = vel[i];
+    const uint32_t idi = (uint32_t)__float_as_int(pi.w);
+    const int cx = cell_coord(pi.x, g.inv_h[0], g.n[0]);
+    const int cy = cell_coord(pi.y, g.inv_h[1], g.n[1]);
+    const int cz = cell_coord(pi.z, g.inv_h[2], g.n[2]);
+    float Fx = 0.0f, Fy = 0.0f, Fz = 0.0f;
+    for (int o = 0; o < 14; ++o) {
+        int jx = cx + c_fwd[o][0], jy = cy + c_fwd[o][1], jz = cz + c_fwd[o][2];
+        float sx = 0.0f, sy = 0.0f, sz = 0.0f;
+        if (jx < 0) { jx += g.n[0]; sx = -g.L[0]; } else if (jx >= g.n[0]) { jx -= g.n[0]; sx = g.L[0]; }
+        if (jy < 0) { jy += g.n[1]; sy = -g.L[1]; } else if (jy >= g.n[1]) { jy -= g.n[1]; sy = g.L[1]; }
+        if (jz < 0) { jz += g.n[2]; sz = -g.L[2]; } else if (jz >= g.n[2]) { jz -= g.n[2]; sz = g.L[2]; }
+        const int c = jx + g.ext[0] * (jy + g.ext[1] * jz);
+        int j0 = start[c];
+        const int j1 = start[c + 1];
+        if (o == 0) j0 = i + 1;
+        for (int j = j0; j < j1; ++j) {
+            const float4 pj = pos[j];
+            const float dx = pi.x - (pj.x + sx);
+            const float dy = pi.y - (pj.y + sy);
+            const float dz = pi.z - (pj.z + sz);
+            const float r2 = dx * dx + dy * dy + dz * dz;
+            if (r2 < pp.rc2 && r2 > 0.0f) {
+                const float4 vj = vel[j];
+                const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
+                const uint32_t idj = (uint32_t)__float_as_int(pj.w);
+                const float s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, s_lo, s_hi);
+                Fx += s * dx;
+                Fy += s * dy;
+                Fz += s * dz;
+                atomic_add_f3(&frc[j], -s * dx, -s * dy, -s * dz);
+                if constexpr (RECORD) {
+                    const unsigned long long k = atomicAdd(rec.count, 1ull);
+                    if ((long long)k < rec.cap) {
+                        const uint2 wd = pair_words(idi, idj, s_lo, s_hi, pp.k0, pp.k1);
+                        rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
+                    }
+                }
+            }
+        }
+    }
+    atomic_add_f3(&frc[i], Fx, Fy, Fz);
+}
+
+// ---------------------------------------------------------------------------------------
+// Output helpers.
+// ---------------------------------------------------------------------------------------
+// Full-step velocity v = u + hk (F + f_body(x)), hk = kick_next - dt/2 (0 right after set).
+__global__ void k_gather_id(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                            const float4 *__restrict__ frc, int n, float hk, float body_f, float x_half,
+                            float3 origin, float *__restrict__ pos3, float *__restrict__ vel3,
+                            float *__restrict__ f3, int by_id)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = pos[i], v = vel[i], f = frc[i];
+    const int row = by_id ? __float_as_int(p.w) : i;
+    if (pos3) {
+        pos3[3 * row + 0] = p.x + origin.x;
+        pos3[3 * row + 1] = p.y + origin.y;
+        pos3[3 * row + 2] = p.z + origin.z;
+    }
+    if (vel3) {
+        const float fb = (p.x <= x_half) ? -body_f : body_f;
+        vel3[3 * row + 0] = __fmaf_rn(hk, f.x, v.x);
+        vel3[3 * row + 1] = __fmaf_rn(hk, f.y, v.y);
+        vel3[3 * row + 2] = __fmaf_rn(hk, __fadd_rn(f.z, fb), v.z);
+    }
+    if (f3) {
+        f3[3 * row + 0] = f.x;
+        f3[3 * row + 1] = f.y;
+        f3[3 * row + 2] = f.z;
+    }
+}
+
+__global__ void k_ids_cells(const float4 *__restrict__ pos, int n, Geom g, int32_t *__restrict__ ids,
+                            int32_t *__restrict__ cell_of_id)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = pos[i];
+    const int id = __float_as_int(p.w);
+    if (ids) ids[i] = id;
+    if (cell_of_id) cell_of_id[id] = cell_index(g, p.x, p.y, p.z);
+}
+
+// Raw-state copy in storage order (x, u, F as float3 rows).
+__global__ void k_state(const float4 *__restrict__ pos, const float4 *__restrict__ vel, const float4 *__restrict__ frc,
+                        int n, float *__restrict__ pos3, float *__restrict__ u3, float *__restrict__ f3,
+                        int32_t *__restrict__ ids)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = pos[i], v = vel[i], f = frc[i];
+    if (pos3) { pos3[3 * i] = p.x; pos3[3 * i + 1] = p.y; pos3[3 * i + 2] = p.z; }
+    if (u3) { u3[3 * i] = v.x; u3[3 * i + 1] = v.y; u3[3 * i + 2] = v.z; }
+    if (f3) { f3[3 * i] = f.x; f3[3 * i + 1] = f.y; f3[3 * i + 2] = f.z; }
+    if (ids) ids[i] = __float_as_int(p.w);
+}
+
+// Philox cross-check kernels (T0 on the device).
+__global__ void k_philox(const uint4 *__restrict__ ctr, const uint2 *__restrict__ key, uint4 *__restrict__ out, int n)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = philox4x32_10(ctr[i], key[i].x, key[i].y);
+}
+
+__global__ void k_pair_words(const uint4 *__restrict__ in, uint2 k, float *__restrict__ xi, uint2 *__restrict__ w,
+                             int n)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint4 q = in[i]; // ida, idb, s_lo, s_hi
+    const uint2 wd = pair_words(q.x, q.y, q.z, q.w, k.x, k.y);
+    w[i] = wd;
+    xi[i] = box_muller(wd.x, wd.y);
+}
+
+} // namespace dpd

@@ -1,0 +1,259 @@
+"""CUDA path (through the C-ABI) against the oracle: parity gate of DESIGN.md §7.
+
+Bars (north_star):
+  * cell indices, per-cell counts, starts and RNG words: bit-exact
+  * per-step forces: |F_gpu - F_oracle|_inf <= 1e-4 max|F| + boundary allowance (C-12)
+  * per-step protocol: the oracle is fed the GPU state of each step (C-13)
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+FORCE_TOL = 1e-4
+
+
+def _ctx(cfg, seed=None):
+    from paper_1911_04712_b200 import capi
+    return capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed if seed is None else seed)
+
+
+def _params(cfg):
+    return oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power,
+                            dt=cfg.dt, seed=cfg.seed, body_f=cfg.body_f)
+
+
+def boundary_eps(box):
+    # fp32 positions near L carry an absolute error of ~ulp(L); widen the C-12 window to it
+    return max(1e-5, 16 * float(np.spacing(np.float32(max(box)))))
+
+
+def by_id(ids, *arrays):
+    order = np.argsort(ids)
+    return [a[order] for a in arrays]
+
+
+def check_forces(F_gpu, F_ref, allow, tol=FORCE_TOL):
+    scale = np.abs(F_ref).max()
+    err = np.abs(F_gpu.astype(np.float64) - F_ref).max(axis=1)
+    bad = err > tol * scale + allow
+    assert not bad.any(), (f"{bad.sum()} particles off; worst {err.max():.3e} vs tol {tol * scale:.3e}; "
+                           f"max allow {allow.max():.3e}")
+    return err.max() / scale
+
+
+def test_device_philox_known_answers():
+    from paper_1911_04712_b200 import capi
+    from conftest import read_golden
+    rows = [[int(t, 16) for t in r] for r in read_golden("philox4x32_10_kat.txt")]
+    ctr = np.array([r[0:4] for r in rows], np.uint32)
+    key = np.array([r[4:6] for r in rows], np.uint32)
+    out = capi.dpd_debug_philox(ctr, key)
+    assert np.array_equal(out, np.array([r[6:10] for r in rows], np.uint32))
+
+
+def test_device_pair_words_and_xi_match_oracle():
+    from paper_1911_04712_b200 import capi
+    rng = np.random.default_rng(11)
+    n = 200000
+    q = np.zeros((n, 4), np.uint32)
+    q[:, 0] = rng.integers(0, 2**31, n)
+    q[:, 1] = rng.integers(0, 2**31, n)
+    steps = rng.integers(0, 2**40, n)
+    q[:, 2] = steps & 0xFFFFFFFF
+    q[:, 3] = steps >> 32
+    words, xi = capi.dpd_debug_pair_words(q, 42)
+    for k in range(0, n, 1999):
+        assert oracle.pair_words(42, int(steps[k]), int(q[k, 0]), int(q[k, 1])) == (int(words[k, 0]), int(words[k, 1]))
+    xi_ref = np.array([oracle.xi(int(a), int(b)) for a, b in words[:20000]])
+    err = np.abs(xi[:20000] - xi_ref)
+    assert err.max() < 2e-3, err.max()          # worst case: u1 -> 1 where sqrt amplifies log error
+    assert np.median(err) < 1e-6
+
+
+def test_hand_placed_pair_worked_values():
+    # SURVEY App. B / tests/golden/pair_worked_values.txt through set_particles + get_forces
+    cfg = workloads.CONFIGS["parity"]
+    d = _ctx(cfg)
+    pos = np.array([[1.0, 1.0, 1.0], [1.5, 1.0, 1.0]], np.float32)
+    vel = np.zeros_like(pos)
+    d.set_particles(pos, vel)
+    f = d.get_forces()
+    np.testing.assert_allclose(f[0], [97.244729631, 0, 0], rtol=2e-6, atol=1e-4)
+    np.testing.assert_allclose(f[1], -f[0], rtol=0, atol=0)
+    # conservative-only and dissipative-only hand examples
+    from paper_1911_04712_b200 import capi
+    d2 = capi.DPD((8.0, 8.0, 8.0), 1.0, 10.0, 0.0, 0.0, 1.0, 0.01, 42)
+    d2.set_particles(np.array([[2.0, 2.0, 2.0], [2.5, 2.0, 2.0]], np.float32), np.zeros((2, 3), np.float32))
+    np.testing.assert_allclose(d2.get_forces()[0], [-5.0, 0, 0], atol=1e-5)
+    d3 = capi.DPD((8.0, 8.0, 8.0), 1.0, 0.0, 4.0, 0.0, 1.0, 0.01, 42)
+    d3.set_particles(np.array([[2.0, 2.0, 2.0], [2.5, 2.0, 2.0]], np.float32),
+                     np.array([[-1.0, 0, 0], [1.0, 0, 0]], np.float32))
+    np.testing.assert_allclose(d3.get_forces()[0], [2.0, 0, 0], atol=1e-5)
+
+
+def test_periodic_boundary_pair_and_degenerates():
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    d = _ctx(cfg)
+    # two particles straddling the periodic boundary in x and z
+    pos = np.array([[0.1, 4.0, 7.95], [7.9, 4.1, 0.05]], np.float32)
+    vel = np.array([[0.3, 0.0, 0.1], [-0.2, 0.1, 0.0]], np.float32)
+    d.set_particles(pos, vel)
+    F_ref, _, npairs = oracle.forces(p, pos, vel, 0)
+    assert npairs == 1
+    np.testing.assert_allclose(d.get_forces(), F_ref, rtol=1e-5, atol=1e-4)
+    # single particle: zero force; N = 0 legal
+    d.set_particles(np.array([[1.0, 2.0, 3.0]], np.float32), np.zeros((1, 3), np.float32))
+    assert np.all(d.get_forces() == 0)
+    d.step(3)
+    d.set_particles(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32))
+    d.step(2)
+    assert d.get_count() == 0 and d.get_step() == 2
+    # positions outside [0, L) are wrapped (C-10)
+    d.set_particles(np.array([[-0.5, 8.0, 17.25]], np.float32), np.zeros((1, 3), np.float32))
+    x, _ = d.get_particles()
+    np.testing.assert_allclose(x[0], [7.5, 0.0, 1.25], atol=1e-6)
+
+
+def test_errors_are_reported():
+    from paper_1911_04712_b200 import capi
+    with pytest.raises(capi.DPDError):
+        capi.DPD((2.0, 8.0, 8.0))  # box < 3 rc
+    with pytest.raises(capi.DPDError):
+        capi.DPD((8.0, 8.0, 8.0), power=1.5)
+    d = capi.DPD((8.0, 8.0, 8.0))
+    pos = np.array([[1.0, np.nan, 1.0]], np.float32)
+    with pytest.raises(capi.DPDError) as e:
+        d.set_particles(pos, np.zeros((1, 3), np.float32))
+    assert e.value.code == capi.DPD_ERR_NUMERIC
+
+
+def test_per_step_parity_config1():
+    """100 steps of config 1 (C-13): each step, the oracle is fed the GPU state."""
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    eps = boundary_eps(cfg.box)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    n = pos0.shape[0]
+    prev = None
+    worst = 0.0
+    kick = 0.5 * cfg.dt
+    for s in range(cfg.steps + 1):
+        pos, u, F, ids = d.get_state()
+        assert d.get_step() == s
+        assert np.array_equal(np.sort(ids), np.arange(n))
+        x_id, u_id, F_id = by_id(ids, pos, u, F)
+        # cells / counts / starts: bit-exact against the fp32 definition (C-8)
+        cell, count, start = d.debug_cells()
+        ocell, ocount, ostart = oracle.cells(p, x_id)
+        assert np.array_equal(count, ocount) and np.array_equal(start, ostart)
+        assert np.array_equal(cell, ocell)
+        # storage order is cell-sorted: cells of consecutive slots are non-decreasing
+        assert np.all(np.diff(ocell[ids]) >= 0)
+        # forces F_s = F(x_s, u_s, s)
+        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps)
+        worst = max(worst, check_forces(F_id, F_ref, allow))
+        # integrator: x_{s} = wrap(x_{s-1} + dt (u_{s-1} + kick F_{s-1})), u_s = u_{s-1} + kick F_{s-1}
+        if prev is not None:
+            px, pu, pF, pk = prev
+            u_pred = pu.astype(np.float64) + pk * pF.astype(np.float64)
+            x_pred = px.astype(np.float64) + cfg.dt * u_pred
+            dx = x_id - x_pred
+            dx -= np.array(cfg.box) * np.rint(dx / np.array(cfg.box))
+            assert np.abs(dx).max() < 2e-6
+            assert np.abs(u_id - u_pred).max() < 1e-5 * (1 + np.abs(u_pred).max())
+        # pair set and RNG words, every 20 steps (T3)
+        if s % 20 == 0:
+            quad = d.debug_pairs()
+            oq, oflag = oracle.pairs(p, x_id, s, eps=eps)
+            gset = {tuple(r) for r in quad.tolist()}
+            core = {tuple(r) for r, f in zip(oq.tolist(), oflag) if (f & 1) and not (f & 2)}
+            boundary = {tuple(r) for r, f in zip(oq.tolist(), oflag) if f & 2}
+            assert len(gset) == len(quad)  # no pair visited twice
+            assert core <= gset
+            assert gset - core <= boundary
+        prev = (x_id, u_id, F_id, kick)
+        kick = cfg.dt
+        if s < cfg.steps:
+            d.step(1)
+    print(f"worst relative force error {worst:.2e}")
+
+
+def test_momentum_and_force_sum():
+    cfg = workloads.CONFIGS["parity"]
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    f = d.get_forces().astype(np.float64)
+    assert np.abs(f.sum(0)).max() < 1e-5 * np.abs(f).sum()
+    _, v0 = d.get_particles()
+    P0 = v0.astype(np.float64).sum(0)
+    d.step(200)
+    _, v = d.get_particles()
+    drift = np.abs(v.astype(np.float64).sum(0) - P0).max()
+    assert drift < 1e-3 * np.abs(v).sum(1).mean() * np.sqrt(len(v)), drift
+
+
+def test_temperature_rho8():
+    # T = kT within 1% (north_star) from full-step velocities (C-14), 16^3 rho=8
+    cfg = workloads.with_box(workloads.CONFIGS["eq64"], (16.0, 16.0, 16.0))
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    d.step(200)
+    Ts = []
+    for _ in range(100):
+        d.step(10)
+        _, v = d.get_particles()
+        Ts.append(oracle.temperature(v))
+    T = float(np.mean(Ts))
+    assert abs(T - cfg.kT) < 0.01 * cfg.kT, T
+
+
+def test_resume_reproduces_rng_words():
+    # checkpoint/resume (C-20): set_particles_ex(ids, step0) continues the same RNG stream
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.CONFIGS["parity"]
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    d.step(7)
+    pos, u, F, ids = d.get_state()
+    d2 = _ctx(cfg)
+    capi.dpd_set_particles_ex(d2.ctx, pos, u, ids, step0=7)
+    F2 = d2.get_forces()
+    x_id, F_id = by_id(ids, pos, F)
+    np.testing.assert_allclose(F2, F_id, rtol=0, atol=2e-4 * np.abs(F_id).max())
+
+
+@pytest.mark.parametrize("name", ["eq64"])
+def test_full_size_sampled_parity(name):
+    """BASELINE config at full size, same launch configuration as bench.py: sampled
+    particles against the oracle's all-j sums, plus size-independent properties."""
+    cfg = workloads.CONFIGS[name]
+    p = _params(cfg)
+    eps = boundary_eps(cfg.box)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    d.step(5)
+    pos, u, F, ids = d.get_state()
+    n = pos.shape[0]
+    assert np.array_equal(np.sort(ids), np.arange(n))
+    rng = np.random.default_rng(0)
+    sel = rng.choice(n, 64, replace=False)
+    F_ref, allow = oracle.forces_subset(p, pos, u, d.get_step(), sel, ids=ids.astype(np.uint32), eps=eps)
+    scale = np.abs(F).max()
+    err = np.abs(F[sel].astype(np.float64) - F_ref).max(axis=1)
+    assert np.all(err <= FORCE_TOL * scale + allow), (err.max(), scale)
+    # cell counts bit-exact at full size
+    cell, count, start = d.debug_cells()
+    _, ocount, ostart = oracle.cells(p, by_id(ids, pos)[0])
+    assert np.array_equal(count, ocount) and np.array_equal(start, ostart)
+    assert np.abs(F.astype(np.float64).sum(0)).max() < 1e-5 * np.abs(F).sum()

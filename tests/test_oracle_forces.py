@@ -126,3 +126,14 @@ def test_pair_enumeration_matches_force_count():
     # words agree with the generator
     for k in range(0, len(quad), 97):
         assert oracle.pair_words(42, 0, int(quad[k, 0]), int(quad[k, 1])) == (int(quad[k, 2]), int(quad[k, 3]))
+
+
+def test_subset_sum_equals_full_sum():
+    # the sampled-parity entry point sums the same pairs as the full brute force
+    p = cfg1()
+    x, v = workloads.make_particles(p.box, 3.0, 1.0)
+    F, allow, _ = oracle.forces(p, x, v, step=2, eps=1e-3)
+    sel = np.array([0, 5, 17, 900, x.shape[0] - 1])
+    Fs, als = oracle.forces_subset(p, x, v, step=2, sel=sel, eps=1e-3)
+    np.testing.assert_allclose(Fs, F[sel], rtol=0, atol=1e-12 * np.abs(F).max())
+    np.testing.assert_allclose(als, allow[sel], rtol=1e-12, atol=1e-15)
