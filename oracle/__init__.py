@@ -69,6 +69,9 @@ def lib():
         P = C.POINTER
         d, u32, i64, dp = C.c_double, C.c_uint32, C.c_int64, P(C.c_double)
         L.oracle_philox4x32_10.argtypes = [P(u32), P(u32), P(u32)]
+        L.oracle_philox2x32_10.argtypes = [P(u32), u32, P(u32)]
+        L.oracle_step_key.argtypes = [C.c_uint64, i64]
+        L.oracle_step_key.restype = u32
         L.oracle_pair_words.argtypes = [C.c_uint64, i64, u32, u32, P(u32)]
         L.oracle_xi.argtypes = [u32, u32]
         L.oracle_xi.restype = d
@@ -123,8 +126,21 @@ def philox4x32_10(ctr, key):
     return o
 
 
+def philox2x32_10(ctr, key: int):
+    """Philox2x32-10 (C-7).  ctr: 2 uint32, key: uint32 -> 2 uint32."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    o = np.zeros(2, dtype=np.uint32)
+    lib().oracle_philox2x32_10(_p(c, C.c_uint32), int(key) & 0xFFFFFFFF, _p(o, C.c_uint32))
+    return o
+
+
+def step_key(seed: int, step: int) -> int:
+    """k_s = word 0 of Philox2x32-10({s lo, s hi}, seed lo ^ seed hi) (C-7)."""
+    return int(lib().oracle_step_key(int(seed), int(step)))
+
+
 def pair_words(seed: int, step: int, ida: int, idb: int):
-    """(w0, w1) of Philox4x32-10(ctr={min id, max id, step lo, step hi}, key=seed) (C-7)."""
+    """(w0, w1) = Philox2x32-10(ctr={min id, max id}, key=k_s) (C-7)."""
     o = np.zeros(2, dtype=np.uint32)
     lib().oracle_pair_words(int(seed), int(step), int(ida), int(idb), _p(o, C.c_uint32))
     return int(o[0]), int(o[1])

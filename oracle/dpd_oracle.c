@@ -11,7 +11,7 @@
  * "S:n" = SPEC.md line n, "C-n" = the reading adopted in DESIGN.md §3.
  *
  * What it computes (all in fp64 unless stated):
- *   - Philox4x32-10 (Random123) counter-based generator                 (C-7)
+ *   - Philox2x32-10 / Philox4x32-10 (Random123) counter-based generators  (C-7)
  *   - per-pair Gaussian xi by Box-Muller on words w0,w1                  (C-7)
  *   - DPD pair force F^C + F^D + F^R                      (eqs. 2-5; C-3..C-5)
  *   - all-pairs O(N^2) minimum-image force sum (the plain definition)    (C-1)
@@ -72,22 +72,45 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* Pair words (C-7): ctr = {min id, max id, step mod 2^32, step >> 32},
- * key = {seed mod 2^32, seed >> 32}; words w0, w1 are used, w2, w3 unused.
- * Symmetric in (ida, idb) by construction: xi_ij = xi_ji. */
+/* Philox2x32-10 (Random123): round (hi, lo) = M * c0; c' = (hi ^ k ^ c1, lo); k += W. */
+static const uint32_t PHILOX2_M = 0xD256D193u, PHILOX2_W = 0x9E3779B9u;
+
+void oracle_philox2x32_10(const uint32_t ctr[2], uint32_t key, uint32_t out[2])
+{
+    uint32_t c0 = ctr[0], c1 = ctr[1], k = key;
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) k += PHILOX2_W;
+        uint64_t p = (uint64_t)PHILOX2_M * (uint64_t)c0;
+        uint32_t hi = (uint32_t)(p >> 32), lo = (uint32_t)p;
+        uint32_t n0 = hi ^ k ^ c1;
+        c0 = n0;
+        c1 = lo;
+    }
+    out[0] = c0;
+    out[1] = c1;
+}
+
+/* Per-step key (C-7): k_s = word 0 of Philox2x32-10(ctr = {s mod 2^32, s >> 32},
+ * key = seed_lo ^ seed_hi). */
+uint32_t oracle_step_key(uint64_t seed, int64_t step)
+{
+    uint32_t ctr[2], out[2];
+    uint64_t s = (uint64_t)step;
+    ctr[0] = (uint32_t)s;
+    ctr[1] = (uint32_t)(s >> 32);
+    oracle_philox2x32_10(ctr, (uint32_t)seed ^ (uint32_t)(seed >> 32), out);
+    return out[0];
+}
+
+/* Pair words (C-7): (w0, w1) = Philox2x32-10(ctr = {min id, max id}, key = k_s).
+ * Symmetric in (ida, idb) by construction: xi_ij = xi_ji; a fresh key per step
+ * makes xi delta-correlated in time. */
 void oracle_pair_words(uint64_t seed, int64_t step, uint32_t ida, uint32_t idb, uint32_t w[2])
 {
-    uint32_t ctr[4], key[2], out[4];
-    uint64_t s = (uint64_t)step;
+    uint32_t ctr[2];
     ctr[0] = ida < idb ? ida : idb;
     ctr[1] = ida < idb ? idb : ida;
-    ctr[2] = (uint32_t)s;
-    ctr[3] = (uint32_t)(s >> 32);
-    key[0] = (uint32_t)seed;
-    key[1] = (uint32_t)(seed >> 32);
-    oracle_philox4x32_10(ctr, key, out);
-    w[0] = out[0];
-    w[1] = out[1];
+    oracle_philox2x32_10(ctr, oracle_step_key(seed, step), w);
 }
 
 /* Box-Muller (C-7): u1 = (w0+1) 2^-32 in (0,1], u2 = w1 2^-32 in [0,1),

@@ -70,12 +70,23 @@ def test_random_term_scaling_fdt():
 
 
 @pytest.mark.parametrize("row", read_golden("pair_worked_values.txt"))
-def test_worked_values_appendix_b(row):
+def test_worked_values(row):
     idi, idj, step = int(row[0]), int(row[1]), int(row[2])
     w0, w1 = int(row[3], 16), int(row[4], 16)
     xi_ref, fx_ref = float(row[5]), float(row[6])
+    # words from the KAT-pinned generator with the C-7 layout
+    ks = int(oracle.philox2x32_10([step & 0xFFFFFFFF, step >> 32], 42)[0])
+    w = oracle.philox2x32_10([min(idi, idj), max(idi, idj)], ks)
+    assert (int(w[0]), int(w[1])) == (w0, w1)
     assert oracle.pair_words(42, step, idi, idj) == (w0, w1)
+    # Box-Muller closed form evaluated independently in Python
+    u1, u2 = (w0 + 1) / 2**32, w1 / 2**32
+    xi_py = math.sqrt(-2 * math.log(u1)) * math.cos(2 * math.pi * u2)
+    assert xi_py == pytest.approx(xi_ref, abs=5e-9)
     assert oracle.xi(w0, w1) == pytest.approx(xi_ref, abs=5e-9)
+    # eq. 3-5 for the hand configuration (r=0.5, e=(-1,0,0), at rest): F_x = -(a w + sigma w^k xi / sqrt(dt))
+    fx_py = -(25.0 * 0.5 + math.sqrt(2 * 45.0 * 1.0) * math.sqrt(0.5) * xi_py / math.sqrt(0.01))
+    assert fx_py == pytest.approx(fx_ref, abs=5e-7)
     p = P(a=25.0, gamma=45.0, kT=1.0, power=0.5, dt=0.01)
     d = oracle.min_image(p, [1.0, 1.0, 1.0], [1.5, 1.0, 1.0])
     f, hit, _ = oracle.pair_force(p, d, [0, 0, 0], idi, idj, step)

@@ -16,6 +16,13 @@ def test_philox_known_answers(row):
     assert [int(o) for o in out] == vals[6:10]
 
 
+@pytest.mark.parametrize("row", read_golden("philox2x32_10_kat.txt"))
+def test_philox2x32_known_answers(row):
+    vals = [int(t, 16) for t in row]
+    out = oracle.philox2x32_10(vals[0:2], vals[2])
+    assert [int(o) for o in out] == vals[3:5]
+
+
 def test_pair_words_symmetric_and_keyed():
     # xi_ij = xi_ji: counter uses (min id, max id)
     for (a, b, s) in [(0, 1, 0), (5, 3, 7), (123456, 99, 2**33 + 5)]:
@@ -25,10 +32,16 @@ def test_pair_words_symmetric_and_keyed():
     assert oracle.pair_words(42, 1, 0, 1) != base
     assert oracle.pair_words(43, 0, 0, 1) != base
     assert oracle.pair_words(42, 0, 0, 2) != base
-    # the counter layout is {lo, hi, step_lo, step_hi}: check against the raw generator
+    # layout (C-7): k_s = Philox2x32-10({s lo, s hi}, seed lo ^ seed hi)[0];
+    # (w0, w1) = Philox2x32-10({min id, max id}, k_s) -- checked against the raw generator
+    seed = (7 << 32) | 42
     s = 2**32 + 17
-    w = oracle.philox4x32_10([3, 9, s & 0xFFFFFFFF, s >> 32], [42, 0])
-    assert oracle.pair_words(42, s, 9, 3) == (int(w[0]), int(w[1]))
+    ks = int(oracle.philox2x32_10([s & 0xFFFFFFFF, s >> 32], 42 ^ 7)[0])
+    assert oracle.step_key(seed, s) == ks
+    w = oracle.philox2x32_10([3, 9], ks)
+    assert oracle.pair_words(seed, s, 9, 3) == (int(w[0]), int(w[1]))
+    # consecutive steps use different keys
+    assert len({oracle.step_key(42, t) for t in range(1000)}) == 1000
 
 
 def test_box_muller_closed_forms():
