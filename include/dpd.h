@@ -71,6 +71,13 @@ const char *dpd_last_error(const dpd_ctx *ctx);
  * non-blocking stream, the default).  The caller keeps ownership of the stream. */
 int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
 
+/* Engine options (name, value):
+ *   "force_kernel" 0 = tiled shared-memory kernel with fixed-point accumulation (default,
+ *                  DESIGN.md §6), 1 = reference thread-per-particle kernel with fp32
+ *                  global atomics (P:276-278 mapping; kept as a cross-check).
+ * Unknown names -> DPD_ERR_ARG. */
+int dpd_set_option(dpd_ctx *ctx, const char *name, int64_t value);
+
 /* Periodic-Poiseuille body force: f_body = (0,0,-f) for r_x <= L_x/2 and
  * (0,0,+f) otherwise (global coordinates).  f = 0 (default) disables it.  The body force
  * enters the integrator, not dpd_get_forces. */
@@ -180,7 +187,7 @@ int dpd_get_forces_ex(dpd_ctx *ctx, int64_t cap, float *f, int32_t *ids, int64_t
 
 /* ---- debug / parity hooks (T0: device RNG against the Random123 known answers) ------- */
 
-/* Run the device Philox4x32-10 on n counters: ctr n x 4, key n x 2, out n x 4 (uint32). */
+/* Run the device Philox2x32-10 (C-7) on n counters: ctr n x 2, key n, out n x 2 (uint32). */
 int dpd_debug_philox(int64_t n, const uint32_t *ctr, const uint32_t *key, uint32_t *out);
 
 /* Device pair words and Box-Muller xi for n (ida, idb, step lo, step hi) quads under seed:

@@ -37,6 +37,7 @@ SIGNATURES = [
     ("dpd_last_error", C.c_char_p, [_vp]),
     ("dpd_set_stream", C.c_int, [_vp, _vp]),
     ("dpd_set_body_force", C.c_int, [_vp, C.c_double]),
+    ("dpd_set_option", C.c_int, [_vp, C.c_char_p, C.c_int64]),
     ("dpd_set_particles", C.c_int, [_vp, C.c_int64, _vp, _vp]),
     ("dpd_set_particles_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_int64]),
     ("dpd_step", C.c_int, [_vp, C.c_int64]),
@@ -122,6 +123,10 @@ def dpd_destroy(ctx):
 
 def dpd_set_stream(ctx, stream_handle):
     _check(ctx, load().dpd_set_stream(ctx, C.c_void_p(stream_handle) if stream_handle else None))
+
+
+def dpd_set_option(ctx, name, value):
+    _check(ctx, load().dpd_set_option(ctx, name.encode(), int(value)))
 
 
 def dpd_set_body_force(ctx, f):
@@ -241,8 +246,9 @@ def dpd_get_launch_count(ctx):
 
 
 def dpd_debug_philox(ctr, key):
-    ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
-    key = np.ascontiguousarray(key, np.uint32).reshape(-1, 2)
+    """Device Philox2x32-10: ctr (n, 2), key (n,) -> (n, 2)."""
+    ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 2)
+    key = np.ascontiguousarray(key, np.uint32).reshape(-1)
     out = np.empty_like(ctr)
     code = load().dpd_debug_philox(ctr.shape[0], _ptr(ctr), _ptr(key), _ptr(out))
     if code != DPD_OK:

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/dpd.h"
+#include "dpd_force_tile.cuh"
 #include "dpd_kernels.cuh"
 
 using namespace dpd;
@@ -69,8 +70,10 @@ struct dpd_ctx {
     uint64_t seed;
     double body_f = 0.0;
     int kmode = 2;
+    int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel
     Geom geom{};
     PairP pp{};
+    FixP fix{};
     float origin[3] = {0, 0, 0};
     // state
     int64_t n = 0;
@@ -256,6 +259,31 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const Geom g = c->geom;
     const PairP pp = c->pp;
+    if (c->force_impl == 0) {
+        const FixP fx = c->fix;
+        const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
+                          ((g.n[2] + FT_BZ - 1) / FT_BZ);
+        const size_t smem = sizeof(ForceTileSmem);
+        return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
+#define DPD_TILE(R, K)                                                                                              \
+    k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, g, pp,  \
+                                                            fx, s_lo, s_hi, rec, c->err.p)
+            if (record) {
+                switch (c->kmode) {
+                case 0: DPD_TILE(true, 0); break;
+                case 1: DPD_TILE(true, 1); break;
+                default: DPD_TILE(true, 2); break;
+                }
+            } else {
+                switch (c->kmode) {
+                case 0: DPD_TILE(false, 0); break;
+                case 1: DPD_TILE(false, 1); break;
+                default: DPD_TILE(false, 2); break;
+                }
+            }
+#undef DPD_TILE
+        });
+    }
     return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
         const unsigned grid = nblk(n, 128);
         if (record) {
@@ -333,9 +361,29 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     pp.inv_rc = (float)(1.0 / rc);
     pp.rc2 = (float)(rc * rc);
     pp.power = (float)power;
-    pp.k0 = (uint32_t)seed;
-    pp.k1 = (uint32_t)(seed >> 32);
+    pp.seed_fold = (uint32_t)seed ^ (uint32_t)(seed >> 32);
     c->pp = pp;
+    // Fixed-point scale of the tiled kernel: bound a single pair's force
+    // magnitude by a + 6.7 sigma/sqrt(dt) (|xi| <= 6.66 with 32-bit u1) + 20 gamma
+    // max(1, sqrt(kT)) (relative speed), keep |f scale| < 2^21; larger magnitudes are
+    // detected on the device and reported as DPD_ERR_NUMERIC.
+    {
+        const double bound = a + 6.7 * (double)pp.sig_dt + 20.0 * gamma * std::max(1.0, std::sqrt(kT)) + 1e-30;
+        int k = (int)std::floor(std::log2(std::ldexp(1.0, 21) / bound));
+        k = std::min(20, std::max(-20, k));
+        c->fix.scale = (float)std::ldexp(1.0, k);
+        c->fix.inv_scale = (float)std::ldexp(1.0, -k);
+        c->fix.mag_lim = (float)std::ldexp(1.0, 21 - k);
+    }
+    {
+        const int smem = (int)sizeof(ForceTileSmem);
+        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
     CUDA_TRY(c, c->err.reserve(4));
@@ -430,6 +478,17 @@ int dpd_set_stream(dpd_ctx *c, void *stream)
         c->own_stream = true;
     }
     return DPD_OK;
+}
+
+int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
+{
+    if (!c || !name) return DPD_ERR_ARG;
+    if (strcmp(name, "force_kernel") == 0) {
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled) or 1 (reference)");
+        c->force_impl = (int)value;
+        return DPD_OK;
+    }
+    return fail(c, DPD_ERR_ARG, "unknown option '%s'", name);
 }
 
 int dpd_set_body_force(dpd_ctx *c, double f)
@@ -690,16 +749,15 @@ int dpd_get_launch_count(const dpd_ctx *c, int64_t *launches)
 int dpd_debug_philox(int64_t n, const uint32_t *ctr, const uint32_t *key, uint32_t *out)
 {
     if (n <= 0) return n == 0 ? DPD_OK : DPD_ERR_ARG;
-    uint4 *dc;
-    uint2 *dk;
-    uint4 *dout;
-    if (cudaMalloc(&dc, sizeof(uint4) * n) != cudaSuccess) return DPD_ERR_CUDA;
-    cudaMalloc(&dk, sizeof(uint2) * n);
-    cudaMalloc(&dout, sizeof(uint4) * n);
-    cudaMemcpy(dc, ctr, sizeof(uint4) * n, cudaMemcpyHostToDevice);
-    cudaMemcpy(dk, key, sizeof(uint2) * n, cudaMemcpyHostToDevice);
-    k_philox<<<nblk(n, 128), 128>>>(dc, dk, dout, (int)n);
-    cudaError_t e = cudaMemcpy(out, dout, sizeof(uint4) * n, cudaMemcpyDeviceToHost);
+    uint2 *dc, *dout;
+    uint32_t *dk;
+    if (cudaMalloc(&dc, sizeof(uint2) * n) != cudaSuccess) return DPD_ERR_CUDA;
+    cudaMalloc(&dk, sizeof(uint32_t) * n);
+    cudaMalloc(&dout, sizeof(uint2) * n);
+    cudaMemcpy(dc, ctr, sizeof(uint2) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(dk, key, sizeof(uint32_t) * n, cudaMemcpyHostToDevice);
+    k_philox2<<<nblk(n, 128), 128>>>(dc, dk, dout, (int)n);
+    cudaError_t e = cudaMemcpy(out, dout, sizeof(uint2) * n, cudaMemcpyDeviceToHost);
     cudaFree(dc);
     cudaFree(dk);
     cudaFree(dout);
@@ -716,7 +774,7 @@ int dpd_debug_pair_words(int64_t n, const uint32_t *quad_in, uint64_t seed, uint
     cudaMalloc(&dw, sizeof(uint2) * n);
     cudaMalloc(&dxi, sizeof(float) * n);
     cudaMemcpy(din, quad_in, sizeof(uint4) * n, cudaMemcpyHostToDevice);
-    k_pair_words<<<nblk(n, 128), 128>>>(din, make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)), dxi, dw, (int)n);
+    k_pair_words<<<nblk(n, 128), 128>>>(din, (uint32_t)seed ^ (uint32_t)(seed >> 32), dxi, dw, (int)n);
     cudaMemcpy(words, dw, sizeof(uint2) * n, cudaMemcpyDeviceToHost);
     cudaError_t e = cudaMemcpy(xi, dxi, sizeof(float) * n, cudaMemcpyDeviceToHost);
     cudaFree(din);

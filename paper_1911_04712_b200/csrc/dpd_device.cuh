@@ -34,8 +34,7 @@ struct PairP {
     float inv_rc;   // 1 / r_c
     float rc2;      // r_c^2
     float power;    // k (w_R = w^k)                                         (C-4)
-    uint32_t k0;    // Philox key words = seed lo, seed hi                   (C-7)
-    uint32_t k1;
+    uint32_t seed_fold; // seed lo ^ seed hi: key of the per-step key          (C-7)
 };
 
 // Integrator parameters (C-2 item 3 / C-6).
@@ -47,47 +46,34 @@ struct IntegP {
 };
 
 // ---------------------------------------------------------------------------------------
-// Philox4x32-10 (C-7).  ctr = {lo id, hi id, step lo, step hi}, key = {k0, k1}.
-// Only output words 0 and 1 are needed, so the 10th round skips the M0 product.
+// Pair RNG (C-7): Philox2x32-10 (Random123).  Round: (hi, lo) = M * c0;
+// c' = (hi ^ k ^ c1, lo); k += W.  Per-step key k_s = Philox2x32-10({s lo, s hi},
+// seed lo ^ seed hi)[0]; pair words (w0, w1) = Philox2x32-10({min id, max id}, k_s).
 // ---------------------------------------------------------------------------------------
-constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
-constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
-constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
-constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+constexpr uint32_t kPhilox2M = 0xD256D193u;
+constexpr uint32_t kPhilox2W = 0x9E3779B9u;
 
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
+__device__ __forceinline__ uint2 philox2x32_10(uint32_t c0, uint32_t c1, uint32_t k)
 {
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(kPhiloxM0, c.x), lo0 = kPhiloxM0 * c.x;
-        const uint32_t hi1 = __umulhi(kPhiloxM1, c.z), lo1 = kPhiloxM1 * c.z;
-        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-        k0 += kPhiloxW0;
-        k1 += kPhiloxW1;
+        const uint32_t hi = __umulhi(kPhilox2M, c0), lo = kPhilox2M * c0;
+        c0 = hi ^ k ^ c1;
+        c1 = lo;
+        k += kPhilox2W;
     }
-    return c;
+    return make_uint2(c0, c1);
 }
 
-// Words (w0, w1) of the pair (ida, idb) at step s.
-__device__ __forceinline__ uint2 pair_words(uint32_t ida, uint32_t idb, uint32_t s_lo, uint32_t s_hi,
-                                            uint32_t k0, uint32_t k1)
+__device__ __forceinline__ uint32_t step_key(uint32_t s_lo, uint32_t s_hi, uint32_t seed_fold)
 {
-    const uint32_t lo = min(ida, idb), hi = max(ida, idb);
-    uint32_t c0 = lo, c1 = hi, c2 = s_lo, c3 = s_hi;
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-        const uint32_t hi0 = __umulhi(kPhiloxM0, c0), lo0 = kPhiloxM0 * c0;
-        const uint32_t hi1 = __umulhi(kPhiloxM1, c2), lo1 = kPhiloxM1 * c2;
-        c0 = hi1 ^ c1 ^ k0;
-        c1 = lo1;
-        c2 = hi0 ^ c3 ^ k1;
-        c3 = lo0;
-        k0 += kPhiloxW0;
-        k1 += kPhiloxW1;
-    }
-    // round 10: outputs 0 and 1 only depend on the M1 product
-    const uint32_t hi1 = __umulhi(kPhiloxM1, c2), lo1 = kPhiloxM1 * c2;
-    return make_uint2(hi1 ^ c1 ^ k0, lo1);
+    return philox2x32_10(s_lo, s_hi, seed_fold).x;
+}
+
+// Words (w0, w1) of the pair (ida, idb) under the per-step key ks.
+__device__ __forceinline__ uint2 pair_words(uint32_t ida, uint32_t idb, uint32_t ks)
+{
+    return philox2x32_10(min(ida, idb), max(ida, idb), ks);
 }
 
 __device__ __forceinline__ float sqrt_approx(float x)
@@ -124,14 +110,14 @@ __device__ __forceinline__ float weight_R(float w, float k)
 // r2 in (0, rc2) assumed.
 template <int KMODE>
 __device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
-                                             uint32_t s_lo, uint32_t s_hi)
+                                             uint32_t ks)
 {
     const float rinv = rsqrtf(r2);
     const float r = r2 * rinv;
     const float w = fmaxf(__fmaf_rn(-r, pp.inv_rc, 1.0f), 0.0f);
     const float wR = weight_R<KMODE>(w, pp.power);
     const float wD = (KMODE == 0) ? w : wR * wR;
-    const uint2 wd = pair_words(idi, idj, s_lo, s_hi, pp.k0, pp.k1);
+    const uint2 wd = pair_words(idi, idj, ks);
     const float xi = box_muller(wd.x, wd.y);
     const float mag = pp.a * w - pp.gamma * wD * (dvdot * rinv) + pp.sig_dt * wR * xi;
     return mag * rinv;

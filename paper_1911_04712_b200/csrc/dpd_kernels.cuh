@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ po
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
     const float4 pi = pos[i], vi = vel[i];
     const uint32_t idi = (uint32_t)__float_as_int(pi.w);
     const int cx = cell_coord(pi.x, g.inv_h[0], g.n[0]);
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ po
                 const float4 vj = vel[j];
                 const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
                 const uint32_t idj = (uint32_t)__float_as_int(pj.w);
-                const float s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, s_lo, s_hi);
+                const float s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks);
                 Fx += s * dx;
                 Fy += s * dy;
                 Fz += s * dz;
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ po
                 if constexpr (RECORD) {
                     const unsigned long long k = atomicAdd(rec.count, 1ull);
                     if ((long long)k < rec.cap) {
-                        const uint2 wd = pair_words(idi, idj, s_lo, s_hi, pp.k0, pp.k1);
+                        const uint2 wd = pair_words(idi, idj, ks);
                         rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
                     }
                 }
@@ -414,19 +415,20 @@ __global__ void k_state(const float4 *__restrict__ pos, const float4 *__restrict
 }
 
 // Philox cross-check kernels (T0 on the device).
-__global__ void k_philox(const uint4 *__restrict__ ctr, const uint2 *__restrict__ key, uint4 *__restrict__ out, int n)
+__global__ void k_philox2(const uint2 *__restrict__ ctr, const uint32_t *__restrict__ key, uint2 *__restrict__ out,
+                          int n)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = philox4x32_10(ctr[i], key[i].x, key[i].y);
+    if (i < n) out[i] = philox2x32_10(ctr[i].x, ctr[i].y, key[i]);
 }
 
-__global__ void k_pair_words(const uint4 *__restrict__ in, uint2 k, float *__restrict__ xi, uint2 *__restrict__ w,
-                             int n)
+__global__ void k_pair_words(const uint4 *__restrict__ in, uint32_t seed_fold, float *__restrict__ xi,
+                             uint2 *__restrict__ w, int n)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint4 q = in[i]; // ida, idb, s_lo, s_hi
-    const uint2 wd = pair_words(q.x, q.y, q.z, q.w, k.x, k.y);
+    const uint2 wd = pair_words(q.x, q.y, step_key(q.z, q.w, seed_fold));
     w[i] = wd;
     xi[i] = box_muller(wd.x, wd.y);
 }

@@ -62,6 +62,34 @@ __global__ void k_ffma(float* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = a + d + e + f + g + h + c;
 }
 
+__global__ void k_ffma2(float* out, int iters) {
+  unsigned long long a = threadIdx.x, b = 0x3f8000003f800000ull, c = 0x3f0000003f000000ull, d = 1, e = 2, f = 3, g = 4, h = 5;
+  for (int k = 0; k < iters; ++k) {
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a) : "l"(b), "l"(c));
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(d) : "l"(b), "l"(c));
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(e) : "l"(b), "l"(c));
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(f) : "l"(b), "l"(c));
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(g) : "l"(b), "l"(c));
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(h) : "l"(b), "l"(c));
+    asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(c) : "l"(b), "l"(d));
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)(a ^ d ^ e ^ f ^ g ^ h ^ c);
+}
+__global__ void k_ffma_mix(float* out, int iters) {  // 4 FFMA + 4 LOP3 per iteration (two pipes)
+  float a = threadIdx.x, b = 1.0001f, c = 0.5f, d = 0.25f; unsigned x = threadIdx.x, y = 7, z = 9, w = 11;
+  for (int k = 0; k < iters; ++k) { a = a * b + c; d = d * b + c; c = c * b + a; b = b * d + a;
+    x = x ^ y ^ k; y = y ^ z ^ x; z = z ^ w ^ y; w = w ^ x ^ z; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a + d + c + b + (float)(x ^ y ^ z ^ w);
+}
+__global__ void k_lds(float* out, int iters) {
+  __shared__ float4 s[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) s[i] = make_float4(i, 1, 2, 3);
+  __syncthreads();
+  float acc = 0.f; int j = threadIdx.x;
+  for (int k = 0; k < iters; ++k) { float4 v = s[(j + k) & 2047]; acc += v.x + v.y; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 int main() {
   const int n = 2 * 1024 * 1024;
   float4* a; int* ai; int* o; float* of; unsigned* ou;
@@ -87,5 +115,8 @@ int main() {
   TIME("I2F x4 (lane-op=I2F)", (k_i2f<<<grid, blk>>>(of, it)), nthr * it * 4);
   TIME("philox round: 2 mulwide (lane-op=round)", (k_imadwide<<<grid, blk>>>(ou, it)), nthr * it);
   TIME("FFMA x7 (lane-op=FFMA)", (k_ffma<<<grid, blk>>>(of, it)), nthr * it * 7);
+  TIME("FFMA2 x7 (lane-op=FFMA2 instr)", (k_ffma2<<<grid, blk>>>(of, it)), nthr * it * 7);
+  TIME("4 FFMA + 4 LOP3 (lane-op=instr)", (k_ffma_mix<<<grid, blk>>>(of, it)), nthr * it * 8);
+  TIME("LDS.128 consecutive (lane-op=LDS)", (k_lds<<<grid, blk>>>(of, it)), nthr * it);
   return 0;
 }
