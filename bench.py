@@ -356,7 +356,8 @@ def main():
            "step_roofline": {"bound": "hbm", "bytes_per_particle_step": BYTES_PER_PARTICLE_STEP,
                              "achieved": step_bytes_gbs, "peak": hbm, "unit": "GB/s",
                              "frac": step_bytes_gbs / hbm, "peak_source": peaks_src},
-           "kernels": per_kernel, "kernel_ms_per_step": step_kernel_ms, "e2e": e2e}
+           "kernels": per_kernel, "kernel_ms_per_step": step_kernel_ms, "e2e": e2e,
+           "force_fallback_tiles": capi.dpd_get_stat(ctx, "fallback_tiles")}
 
     if rank == 0 and not args.no_cpu_baseline:
         try:

@@ -14,8 +14,8 @@
  *     F^C = a w e, w = 1 - r/r_c;  F^D = -gamma w_D (v_ij.e) e;
  *     F^R = sigma xi_ij w_R e / sqrt(dt);  w_R = w^k, w_D = w_R^2,
  *     sigma^2 = 2 gamma kT                                               (C-3, C-4)
- *   - xi_ij from Philox4x32-10(ctr = {min id, max id, step lo, step hi},
- *     key = {seed lo, seed hi}), Box-Muller on words 0,1                  (C-7)
+ *   - xi_ij by Box-Muller on (w0, w1) = Philox2x32-10(ctr = {min id, max id}, key = k_s),
+ *     k_s = word 0 of Philox2x32-10({step lo, step hi}, seed lo ^ seed hi) (C-7)
  *   - cell lists of edge >= r_c rebuilt every step
  *   - "fused Velocity-Verlet" = Groot-Warren VV, lambda = 1/2             (C-6)
  *   - 3D domain decomposition with ghost exchange and redistribution
@@ -77,6 +77,11 @@ int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
  *                  global atomics (P:276-278 mapping; kept as a cross-check).
  * Unknown names -> DPD_ERR_ARG. */
 int dpd_set_option(dpd_ctx *ctx, const char *name, int64_t value);
+
+/* Engine statistics (cumulative since creation): "fallback_tiles" = tiles of the tiled
+ * force kernel that exceeded a shared-memory capacity and were evaluated by its global-memory
+ * fallback ("fallback_staged", "fallback_home", "fallback_list" split it by cause). */
+int dpd_get_stat(dpd_ctx *ctx, const char *name, int64_t *value);
 
 /* Periodic-Poiseuille body force: f_body = (0,0,-f) for r_x <= L_x/2 and
  * (0,0,+f) otherwise (global coordinates).  f = 0 (default) disables it.  The body force

@@ -38,6 +38,7 @@ SIGNATURES = [
     ("dpd_set_stream", C.c_int, [_vp, _vp]),
     ("dpd_set_body_force", C.c_int, [_vp, C.c_double]),
     ("dpd_set_option", C.c_int, [_vp, C.c_char_p, C.c_int64]),
+    ("dpd_get_stat", C.c_int, [_vp, C.c_char_p, _P(C.c_int64)]),
     ("dpd_set_particles", C.c_int, [_vp, C.c_int64, _vp, _vp]),
     ("dpd_set_particles_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_int64]),
     ("dpd_step", C.c_int, [_vp, C.c_int64]),
@@ -127,6 +128,12 @@ def dpd_set_stream(ctx, stream_handle):
 
 def dpd_set_option(ctx, name, value):
     _check(ctx, load().dpd_set_option(ctx, name.encode(), int(value)))
+
+
+def dpd_get_stat(ctx, name):
+    v = C.c_int64()
+    _check(ctx, load().dpd_get_stat(ctx, name.encode(), C.byref(v)))
+    return v.value
 
 
 def dpd_set_body_force(ctx, f):

@@ -97,6 +97,7 @@ struct dpd_ctx {
     double t_ms[KID_COUNT] = {0};
     int64_t t_launches[KID_COUNT] = {0};
     int64_t launches = 0;
+    int64_t fallback[3] = {0, 0, 0}; // tiled-kernel fallbacks: staged / home / list capacity
     std::string last_error;
 };
 
@@ -180,9 +181,14 @@ int resolve_timing(dpd_ctx *c)
 // Synchronise and translate the device error word.
 int sync_check(dpd_ctx *c)
 {
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     resolve_timing(c);
+    if (c->h_err[4] | c->h_err[5] | c->h_err[6]) {
+        for (int k = 0; k < 3; ++k) c->fallback[k] += c->h_err[4 + k];
+        CUDA_TRY(c, cudaMemsetAsync(c->err.p + 4, 0, 4 * sizeof(int), c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    }
     if (c->h_err[0] != 0) {
         const int flags = c->h_err[0], id = c->h_err[1];
         cudaMemsetAsync(c->err.p, 0, 4 * sizeof(int), c->stream);
@@ -376,19 +382,22 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
         c->fix.mag_lim = (float)std::ldexp(1.0, 21 - k);
     }
     {
+        // two tiles per SM need the maximum shared-memory carveout (2 x (smem + 1 KB) <= 228 KB)
         const int smem = (int)sizeof(ForceTileSmem);
-        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_force_tile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const void *fns[6] = {(const void *)k_force_tile<false, 0>, (const void *)k_force_tile<false, 1>,
+                              (const void *)k_force_tile<false, 2>, (const void *)k_force_tile<true, 0>,
+                              (const void *)k_force_tile<true, 1>,  (const void *)k_force_tile<true, 2>};
+        for (const void *f : fns) {
+            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared));
+        }
     }
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
-    CUDA_TRY(c, c->err.reserve(4));
-    CUDA_TRY(c, cudaMemset(c->err.p, 0, 4 * sizeof(int)));
-    CUDA_TRY(c, cudaMallocHost(&c->h_err, 4 * sizeof(int)));
+    CUDA_TRY(c, c->err.reserve(8));
+    CUDA_TRY(c, cudaMemset(c->err.p, 0, 8 * sizeof(int)));
+    CUDA_TRY(c, cudaMallocHost(&c->h_err, 8 * sizeof(int)));
     CUDA_TRY(c, c->scan_epoch.reserve(1));
     CUDA_TRY(c, cudaMemset(c->scan_epoch.p, 0, sizeof(unsigned)));
     return DPD_OK;
@@ -489,6 +498,20 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
         return DPD_OK;
     }
     return fail(c, DPD_ERR_ARG, "unknown option '%s'", name);
+}
+
+int dpd_get_stat(dpd_ctx *c, const char *name, int64_t *value)
+{
+    if (!c || !name || !value) return DPD_ERR_ARG;
+    TRY(sync_check(c));
+    if (strcmp(name, "fallback_tiles") == 0) {
+        *value = c->fallback[0] + c->fallback[1] + c->fallback[2];
+        return DPD_OK;
+    }
+    if (strcmp(name, "fallback_staged") == 0) { *value = c->fallback[0]; return DPD_OK; }
+    if (strcmp(name, "fallback_home") == 0) { *value = c->fallback[1]; return DPD_OK; }
+    if (strcmp(name, "fallback_list") == 0) { *value = c->fallback[2]; return DPD_OK; }
+    return fail(c, DPD_ERR_ARG, "unknown statistic '%s'", name);
 }
 
 int dpd_set_body_force(dpd_ctx *c, double f)

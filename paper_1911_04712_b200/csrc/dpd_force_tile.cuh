@@ -3,19 +3,22 @@
 // One CTA per tile of BX x BY x BZ home cells (cell lists, symmetric forces):
 //   1. stage   : the tile's forward half-stencil region, (BX+2) x (BY+2) x (BZ+1) cells,
 //                is copied row by row (contiguous global ranges) into shared memory, with
-//                periodic images pre-shifted into the tile frame;
-//   2. scan    : each lane owns one home particle i and sweeps its 5 contiguous smem
-//                segments (own cell after i + next cell, the y+1 row, three z+1 rows),
-//                appending in-cutoff j to a private list -- 2 predicated instructions per
-//                candidate, no divergent pair body;
-//   3. pairs   : the warp evaluates the concatenated lists 32 pairs at a time (full SIMT
-//                efficiency), the owner lane found by a shuffle binary search over the
-//                list prefix sums;
+//                periodic images pre-shifted into the tile frame (AoS float4 + an SoA copy
+//                of x, y, z for the packed sweep);
+//   2. sweep   : thread h owns home particle h and sweeps its 5 contiguous smem segments
+//                (own cell after i + next cell, the y+1 row, three z+1 rows) two candidates
+//                at a time with packed fp32x2 arithmetic (FADD2/FFMA2), appending in-cutoff
+//                j to the particle's list -- one predicated store + add per hit;
+//   3. pairs   : the CTA-wide concatenation of all lists is cut into NTHR contiguous chunks
+//                (perfect load balance across warps); a chunk spans one or two owners, so the
+//                i-side sum stays in registers;
 //   4. accumulate: f is quantised once to 32-bit fixed point and added with native
 //                shared-memory integer atomics (+q on i, -q on j): exact Newton-3,
 //                order-independent sums;
 //   5. flush   : every staged particle's sum is converted back to fp32 and added to the
 //                global force array with one vector reduction (REDG.F32x4).
+// Tiles whose particle counts exceed the shared-memory capacities (never seen at rho = 8,
+// > 9 sigma) are evaluated by a direct global-memory fallback with the same pair function.
 #pragma once
 
 #include "dpd_kernels.cuh"
@@ -25,13 +28,13 @@ namespace dpd {
 constexpr int FT_BX = 4, FT_BY = 4, FT_BZ = 2;
 constexpr int FT_SX = FT_BX + 2, FT_SY = FT_BY + 2, FT_SZ = FT_BZ + 1;
 constexpr int FT_NSC = FT_SX * FT_SY * FT_SZ; // staged cells (108)
-constexpr int FT_NROW = FT_SY * FT_SZ;        // staged rows (18)
 constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
-constexpr int FT_NTHR = 288;                 // > mean home count (256): no straggler rounds
-constexpr int FT_SCAP = 1280;                 // staged particles (mean 864 at rho = 8)
-constexpr int FT_LCAP = 48;                   // per-lane pair-list capacity
-constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 25 words per lane (odd): conflict-free appends
+constexpr int FT_NTHR = 288;                  // > mean home count (256)
 constexpr int FT_NWARP = FT_NTHR / 32;
+constexpr int FT_SCAP = 1152;                 // staged particles (mean 864, sd 29 at rho = 8)
+constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
+constexpr int FT_LCAP = 48;                   // hits per home particle (mean 16.8)
+constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 25 words per list (odd): conflict-free appends
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
 struct FixP {
@@ -41,18 +44,25 @@ struct FixP {
 };
 
 struct ForceTileSmem {
-    float4 sp[FT_SCAP];                        // staged positions (tile frame), w = id bits
-    float4 sv[FT_SCAP];                        // staged velocities
-    float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // SoA copy of the positions for the f32x2 sweep
-    int acc[3][FT_SCAP];                       // fixed-point force sums
-    int gidx[FT_SCAP];                         // slot in the global sorted arrays
-    unsigned short lst[FT_NTHR * FT_LSTRIDE];  // per-lane pair lists (lane-major, padded)
-    int soff[FT_NSC + 1];                      // staged cell -> smem start (exclusive scan)
-    int cgs[FT_NSC];                           // staged cell -> global start
-    int hoff[FT_NHROW + 1];                    // home row -> first home index (prefix)
-    int wexcl[FT_NWARP][33];                   // per-warp list prefix sums (+ total)
-    int wsi[FT_NWARP][32];                     // per-warp owner smem indices
-    int total;
+    float4 sp[FT_SCAP];                          // staged positions (tile frame), w = id bits
+    float4 sv[FT_SCAP];                          // staged velocities
+    float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // SoA copy of the positions for the sweep
+    int acc[3][FT_SCAP];                         // fixed-point force sums
+    unsigned short lst[FT_HCAP * FT_LSTRIDE];    // per-home-particle pair lists
+    int oexcl[FT_HCAP + 1];                      // compacted owners: list prefix (+ total)
+    int osi[FT_HCAP];                            //   staged index of the owner
+    int orow[FT_HCAP];                           //   list base minus prefix
+    int hcnt[FT_HCAP];                           // hits per home particle
+    int hsi[FT_HCAP];                            // staged index per home particle
+    int soff[FT_NSC + 1];                        // staged cell -> smem start (exclusive scan)
+    int cgs[FT_NSC];                             // staged cell -> global start
+    int scnt[FT_NSC];                            // staged cell -> particle count
+    int hoff[FT_NHROW + 1];                      // home row -> first home index (prefix)
+    int wsum[FT_NWARP];                          // block-scan scratch
+    int tile[4];                                 // x0, y0, z0 of this tile
+    int total;                                   // staged particles
+    int nown;                                    // owners with a non-empty list
+    int overflow;                                // a capacity was exceeded -> fallback
 };
 
 __device__ __forceinline__ int to_fixed(float f, float scale)
@@ -61,102 +71,10 @@ __device__ __forceinline__ int to_fixed(float f, float scale)
     return __float_as_int(__fmaf_rn(f, scale, 12582912.0f)) - 0x4B400000;
 }
 
-// Pair-list evaluation for one warp.  Lanes hold (cnt, s_i) of their own home particle; the
-// 32 lists form one flat sequence of `total` pairs, cut into 32 contiguous chunks of
-// C = ceil(total / 32): lane k evaluates entries [k C, (k+1) C).  A chunk spans one or two
-// owners, so the i-side sum stays in registers and is flushed with one atomic per owner
-// change, and in any iteration the 32 lanes touch 32 different owners (no same-address
-// atomics).  The j side is one fixed-point shared atomic per component.
-template <bool RECORD, int KMODE>
-__device__ __forceinline__ void tile_pairs(ForceTileSmem &S, int lane, int tid, int cnt, int s_i, const PairP &pp,
-                                           const FixP &fx, uint32_t ks, PairRec &rec, int *err)
-{
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) return;
-    const int excl = incl - cnt;
-    const int wbase = tid - lane;
-    const int warp = tid >> 5;
-    S.wexcl[warp][lane] = excl;
-    S.wsi[warp][lane] = s_i;
-    if (lane == 0) S.wexcl[warp][32] = total;
-    const int C = (total + 31) >> 5;
-    const int t0 = lane * C;
-    const int t1 = min(t0 + C, total);
-    // owner of t0: largest lane o with excl_o <= t0
-    int o = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-        const int e = __shfl_sync(0xffffffffu, excl, o + step);
-        if (e <= t0) o += step;
-    }
-    __syncwarp();
-    int eo = S.wexcl[warp][o], enext = S.wexcl[warp][o + 1];
-    int si = S.wsi[warp][o];
-    float4 pi = S.sp[si], vi = S.sv[si];
-    int fx_i = 0, fy_i = 0, fz_i = 0;
-    for (int r = 0; r < C; ++r) {
-        const int t = t0 + r;
-        if (t >= t1) break;
-        if (t >= enext) { // next owner: flush the i-side sum
-            atomicAdd(&S.acc[0][si], fx_i);
-            atomicAdd(&S.acc[1][si], fy_i);
-            atomicAdd(&S.acc[2][si], fz_i);
-            fx_i = fy_i = fz_i = 0;
-            eo = enext;
-            ++o;
-            enext = S.wexcl[warp][o + 1];
-            while (enext <= t) { // skip owners with empty lists (rare)
-                ++o;
-                enext = S.wexcl[warp][o + 1];
-            }
-            si = S.wsi[warp][o];
-            pi = S.sp[si];
-            vi = S.sv[si];
-        }
-        const int j = S.lst[(wbase + o) * FT_LSTRIDE + (t - eo)];
-        const float4 pj = S.sp[j], vj = S.sv[j];
-        const float dx = pi.x - pj.x, dy = pi.y - pj.y, dz = pi.z - pj.z;
-        const float r2 = dx * dx + dy * dy + dz * dz;
-        const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
-        const uint32_t idi = (uint32_t)__float_as_int(pi.w), idj = (uint32_t)__float_as_int(pj.w);
-        float s = 0.0f;
-        if (r2 > 0.0f) {
-            s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks);
-            if (fabsf(s) * (r2 * rsqrtf(r2)) > fx.mag_lim) raise_err(err, ERR_RANGE, (int)idi);
-            if constexpr (RECORD) {
-                const unsigned long long k = atomicAdd(rec.count, 1ull);
-                if ((long long)k < rec.cap) {
-                    const uint2 wd = pair_words(idi, idj, ks);
-                    rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
-                }
-            }
-        }
-        const int qx = to_fixed(s * dx, fx.scale);
-        const int qy = to_fixed(s * dy, fx.scale);
-        const int qz = to_fixed(s * dz, fx.scale);
-        fx_i += qx;
-        fy_i += qy;
-        fz_i += qz;
-        atomicAdd(&S.acc[0][j], -qx); // native ATOMS.ADD (the fp32 variant is a CAS loop)
-        atomicAdd(&S.acc[1][j], -qy);
-        atomicAdd(&S.acc[2][j], -qz);
-    }
-    if (t0 < t1) {
-        atomicAdd(&S.acc[0][si], fx_i);
-        atomicAdd(&S.acc[1][si], fy_i);
-        atomicAdd(&S.acc[2][si], fz_i);
-    }
-    __syncwarp();
-}
-
-// Candidate sweep helpers.  The list pointer `lptr` is a shared-memory byte address; an
+// ---------------------------------------------------------------------------------------
+// Sweep helpers.  `lptr` is a shared-memory byte address into the particle's list; an
 // in-cutoff candidate j costs one predicated 16-bit store and one predicated add.
+// ---------------------------------------------------------------------------------------
 __device__ __forceinline__ void append_if(unsigned &lptr, float r2, float rc2, unsigned j)
 {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\t@p st.shared.u16 [%0], %3;\n\t"
@@ -232,10 +150,196 @@ __device__ __forceinline__ void stage_segment(ForceTileSmem &S, const float4 *__
         S.sy[s] = py;
         S.sz[s] = pz;
         S.sv[s] = vel[g0 + k];
-        S.gidx[s] = g0 + k;
         S.acc[0][s] = 0;
         S.acc[1][s] = 0;
         S.acc[2][s] = 0;
+    }
+}
+
+// Block-wide exclusive scan of one int per thread (FT_NTHR threads); returns the total.
+__device__ __forceinline__ int block_excl_scan(ForceTileSmem &S, int v, int &excl, int lane, int warp)
+{
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.wsum[warp] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < FT_NWARP; ++w) {
+        const int s = S.wsum[w];
+        before += (w < warp) ? s : 0;
+        total += s;
+    }
+    excl = before + incl - v;
+    return total;
+}
+
+// Pair evaluation shared by the fast path (smem operands) and the record path.
+template <bool RECORD, int KMODE>
+__device__ __forceinline__ float pair_eval(const PairP &pp, const FixP &fx, float4 pi, float4 vi, float4 pj,
+                                           float4 vj, uint32_t ks, PairRec &rec, int *err, float &dx, float &dy,
+                                           float &dz)
+{
+    dx = pi.x - pj.x;
+    dy = pi.y - pj.y;
+    dz = pi.z - pj.z;
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
+    const uint32_t idi = (uint32_t)__float_as_int(pi.w), idj = (uint32_t)__float_as_int(pj.w);
+    float s = 0.0f;
+    if (r2 > 0.0f) {
+        s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks);
+        if (fabsf(s) * (r2 * rsqrtf(r2)) > fx.mag_lim) raise_err(err, ERR_RANGE, (int)idi);
+        if constexpr (RECORD) {
+            const unsigned long long k = atomicAdd(rec.count, 1ull);
+            if ((long long)k < rec.cap) {
+                const uint2 wd = pair_words(idi, idj, ks);
+                rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
+            }
+        }
+    }
+    return s;
+}
+
+// Branch-free pair force: f_ij = s (dx, dy, dz); s = 0 for coincident particles (C-11).
+template <int KMODE>
+__device__ __forceinline__ float pair_core(const PairP &pp, float4 pi, float4 vi, float4 pj, float4 vj, uint32_t ks,
+                                           float &dx, float &dy, float &dz)
+{
+    dx = pi.x - pj.x;
+    dy = pi.y - pj.y;
+    dz = pi.z - pj.z;
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
+    const float s = pair_scalar<KMODE>(pp, fmaxf(r2, 1e-30f), dvdot, (uint32_t)__float_as_int(pi.w),
+                                       (uint32_t)__float_as_int(pj.w), ks);
+    return r2 > 0.0f ? s : 0.0f;
+}
+
+// Range check of the fixed-point conversion and (debug) pair recording.
+template <bool RECORD>
+__device__ __forceinline__ void pair_checks(const PairP &pp, const FixP &fx, float4 pi, float4 pj, float s, float dx,
+                                            float dy, float dz, uint32_t ks, PairRec &rec, int *err)
+{
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    if (fabsf(s) * (r2 * rsqrtf(fmaxf(r2, 1e-30f))) > fx.mag_lim) raise_err(err, ERR_RANGE, __float_as_int(pi.w));
+    if constexpr (RECORD) {
+        if (r2 > 0.0f) {
+            const uint32_t idi = (uint32_t)__float_as_int(pi.w), idj = (uint32_t)__float_as_int(pj.w);
+            const unsigned long long k = atomicAdd(rec.count, 1ull);
+            if ((long long)k < rec.cap) {
+                const uint2 wd = pair_words(idi, idj, ks);
+                rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
+            }
+        }
+    }
+}
+
+// Walk over a contiguous range [t, t1) of the CTA-wide pair list.  Owners (home particles
+// with a non-empty list) change at most a few times per range; the i-side fixed-point sum
+// is kept in registers and flushed on each owner change.
+struct PairCursor {
+    int t, t1, o, enext, si, lrow;
+    float4 pi, vi;
+    int fx, fy, fz;
+};
+
+__device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &S, int t0, int t1, int nown)
+{
+    c.t = t0;
+    c.t1 = t1;
+    c.fx = c.fy = c.fz = 0;
+    int o = 0; // largest owner slot with oexcl[o] <= t0
+#pragma unroll
+    for (int step = 256; step > 0; step >>= 1)
+        if (o + step < nown && S.oexcl[o + step] <= t0) o += step;
+    c.o = o;
+    c.enext = S.oexcl[o + 1];
+    c.si = S.osi[o];
+    c.lrow = S.orow[o];
+    c.pi = S.sp[c.si];
+    c.vi = S.sv[c.si];
+}
+
+__device__ __forceinline__ void cursor_flush(PairCursor &c, ForceTileSmem &S)
+{
+    if (c.fx | c.fy | c.fz) {
+        atomicAdd(&S.acc[0][c.si], c.fx);
+        atomicAdd(&S.acc[1][c.si], c.fy);
+        atomicAdd(&S.acc[2][c.si], c.fz);
+    }
+    c.fx = c.fy = c.fz = 0;
+}
+
+// Entry t of the list (the partner j); moves to the next owner first when t crosses it.
+__device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
+{
+    if (c.t >= c.enext) { // next owner (never empty)
+        cursor_flush(c, S);
+        ++c.o;
+        c.enext = S.oexcl[c.o + 1];
+        c.si = S.osi[c.o];
+        c.lrow = S.orow[c.o];
+        c.pi = S.sp[c.si];
+        c.vi = S.sv[c.si];
+    }
+    return S.lst[c.lrow + c.t];
+}
+
+__device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &S, int j, float s, float dx, float dy,
+                                                  float dz, float scale)
+{
+    const int qx = to_fixed(s * dx, scale), qy = to_fixed(s * dy, scale), qz = to_fixed(s * dz, scale);
+    c.fx += qx;
+    c.fy += qy;
+    c.fz += qz;
+    atomicAdd(&S.acc[0][j], -qx); // native ATOMS.ADD (the fp32 variant is a CAS loop)
+    atomicAdd(&S.acc[1][j], -qy);
+    atomicAdd(&S.acc[2][j], -qz);
+    ++c.t;
+}
+
+// Direct global-memory evaluation of one tile's home cells (capacity overflow only).
+template <bool RECORD, int KMODE>
+__device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *frc,
+                              const int *__restrict__ start, const Geom &g, const PairP &pp, const FixP &fx,
+                              uint32_t ks, PairRec &rec, int *err, int x0, int y0, int z0, int bx, int by, int bz)
+{
+    for (int hc = 0; hc < bx * by * bz; ++hc) {
+        const int cx = x0 + hc % bx, cy = y0 + (hc / bx) % by, cz = z0 + hc / (bx * by);
+        const int c0 = cx + g.ext[0] * (cy + g.ext[1] * cz);
+        for (int i = start[c0] + threadIdx.x; i < start[c0 + 1]; i += FT_NTHR) {
+            const float4 pi = pos[i], vi = vel[i];
+            float Fx = 0.f, Fy = 0.f, Fz = 0.f;
+            for (int o = 0; o < 14; ++o) {
+                int jx = cx + c_fwd[o][0], jy = cy + c_fwd[o][1], jz = cz + c_fwd[o][2];
+                float sx = 0.f, sy = 0.f, sz = 0.f;
+                if (jx < 0) { jx += g.n[0]; sx = -g.L[0]; } else if (jx >= g.n[0]) { jx -= g.n[0]; sx = g.L[0]; }
+                if (jy < 0) { jy += g.n[1]; sy = -g.L[1]; } else if (jy >= g.n[1]) { jy -= g.n[1]; sy = g.L[1]; }
+                if (jz >= g.n[2]) { jz -= g.n[2]; sz = g.L[2]; }
+                const int c = jx + g.ext[0] * (jy + g.ext[1] * jz);
+                for (int j = (o == 0 ? i + 1 : start[c]); j < start[c + 1]; ++j) {
+                    float4 pj = pos[j];
+                    pj.x += sx;
+                    pj.y += sy;
+                    pj.z += sz;
+                    float dx, dy, dz;
+                    const float r2 = (pi.x - pj.x) * (pi.x - pj.x) + (pi.y - pj.y) * (pi.y - pj.y) +
+                                     (pi.z - pj.z) * (pi.z - pj.z);
+                    if (!(r2 < pp.rc2)) continue;
+                    const float s = pair_eval<RECORD, KMODE>(pp, fx, pi, vi, pj, vel[j], ks, rec, err, dx, dy, dz);
+                    Fx += s * dx;
+                    Fy += s * dy;
+                    Fz += s * dz;
+                    atomicAdd(&frc[j], make_float4(-s * dx, -s * dy, -s * dz, 0.0f));
+                }
+            }
+            atomicAdd(&frc[i], make_float4(Fx, Fy, Fz, 0.0f));
+        }
     }
 }
 
@@ -248,26 +352,41 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
 
-    // ---- tile geometry ---------------------------------------------------------------
-    const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
-    const int tx = blockIdx.x % ntx, ty = (blockIdx.x / ntx) % nty, tz = blockIdx.x / (ntx * nty);
-    const int x0 = tx * FT_BX, y0 = ty * FT_BY, z0 = tz * FT_BZ;
+    // ---- tile geometry (integer divisions once per CTA) --------------------------------
+    static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
+    if (tid == 0) {
+        const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
+        const int b = blockIdx.x;
+        S.tile[0] = (b % ntx) * FT_BX;
+        S.tile[1] = ((b / ntx) % nty) * FT_BY;
+        S.tile[2] = (b / (ntx * nty)) * FT_BZ;
+        S.overflow = 0;
+    }
+    __syncthreads();
+    const int x0 = S.tile[0], y0 = S.tile[1], z0 = S.tile[2];
     const int bx = min(FT_BX, g.n[0] - x0), by = min(FT_BY, g.n[1] - y0), bz = min(FT_BZ, g.n[2] - z0);
     const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
     const int nsc = sxa * sya * sza;
 
     // ---- 1a. staged cell table (counts, then one-warp exclusive scan) -----------------
-    for (int c = tid; c < nsc; c += FT_NTHR) {
-        const int lx = c % sxa, ly = (c / sxa) % sya, lz = c / (sxa * sya);
-        int gx = x0 - 1 + lx, gy = y0 - 1 + ly, gz = z0 + lz;
-        gx += (gx < 0) ? g.n[0] : (gx >= g.n[0] ? -g.n[0] : 0);
+    for (int row = warp; row < sya * sza; row += FT_NWARP) {
+        const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0); // sza <= 3
+        const int ly = row - lz * sya;
+        int gy = y0 - 1 + ly, gz = z0 + lz;
         gy += (gy < 0) ? g.n[1] : (gy >= g.n[1] ? -g.n[1] : 0);
         gz += (gz >= g.n[2]) ? -g.n[2] : 0;
-        const int gc = gx + g.ext[0] * (gy + g.ext[1] * gz);
-        const int a = start[gc];
-        S.cgs[c] = a;
-        S.soff[c] = start[gc + 1] - a;
+        if (lane < sxa) {
+            int gx = x0 - 1 + lane;
+            gx += (gx < 0) ? g.n[0] : (gx >= g.n[0] ? -g.n[0] : 0);
+            const int gc = gx + g.ext[0] * (gy + g.ext[1] * gz);
+            const int a = start[gc];
+            const int c = row * sxa + lane;
+            S.cgs[c] = a;
+            S.soff[c] = start[gc + 1] - a;
+            S.scnt[c] = start[gc + 1] - a;
+        }
     }
     __syncthreads();
     if (warp == 0) {
@@ -296,28 +415,32 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
             S.soff[nsc] = incl;
             S.total = incl;
         }
+    } else if (warp == 1 && lane == 0) {
+        // home rows (ly = 1..by, lz = 0..bz-1), cells lx = 1..bx: prefix of their sizes
+        // (from the counts; the in-place scan of soff runs concurrently in warp 0)
+        int run = 0;
+        for (int r = 0; r < by * bz; ++r) {
+            const int lz = r >= by ? 1 : 0;
+            const int ly = 1 + r - lz * by;
+            const int c = 1 + sxa * (ly + sya * lz);
+            S.hoff[r] = run;
+            for (int x = 0; x < bx; ++x) run += S.scnt[c + x];
+        }
+        S.hoff[by * bz] = run;
     }
     __syncthreads();
     const int total = S.total;
-    if (total > FT_SCAP) {
-        if (tid == 0) raise_err(err, ERR_CAPACITY, total);
+    const int nhome = S.hoff[by * bz];
+    if (total > FT_SCAP || nhome > FT_HCAP) {
+        if (tid == 0) atomicAdd(&err[total > FT_SCAP ? 4 : 5], 1); // fallback statistics
+        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, x0, y0, z0, bx, by, bz);
         return;
-    }
-    if (warp == 1 && lane == 0) {
-        // home rows (ly = 1..by, lz = 0..bz-1), cells lx = 1..bx: prefix of their sizes
-        int run = 0;
-        for (int r = 0; r < by * bz; ++r) {
-            const int ly = 1 + r % by, lz = r / by;
-            const int c = 1 + sxa * (ly + sya * lz);
-            S.hoff[r] = run;
-            run += S.soff[c + bx] - S.soff[c];
-        }
-        S.hoff[by * bz] = run;
     }
 
     // ---- 1b. stage rows: each row is <= 3 contiguous global segments -----------------
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
-        const int ly = row % sya, lz = row / sya;
+        const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0);
+        const int ly = row - lz * sya;
         const int gy = y0 - 1 + ly, gz = z0 + lz;
         const float sy = gy < 0 ? -g.L[1] : (gy >= g.n[1] ? g.L[1] : 0.0f);
         const float sz = gz >= g.n[2] ? g.L[2] : 0.0f;
@@ -335,72 +458,136 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
     }
     __syncthreads();
 
-    // ---- 2 + 3. per-lane candidate sweep, then warp-balanced pair evaluation ----------
-    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
-    const int nhome = S.hoff[by * bz];
-    const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[tid * FT_LSTRIDE]);
+    // ---- 2. sweep: one home particle per thread (a second round only past FT_NTHR) -------
     const int rowz = sxa * sya;
-    for (int h0 = warp * 32; h0 < nhome; h0 += FT_NTHR) {
-        const int h = h0 + lane;
-        int s_i = 0, cnt = 0;
-        int lo[5], hi[5];
-        float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) lo[k] = hi[k] = 0;
-        if (h < nhome) {
-            int r = 0;
-            while (r + 1 < by * bz && S.hoff[r + 1] <= h) ++r;
-            const int ly = 1 + r % by, lz = r / by;
-            const int crow = sxa * (ly + sya * lz);
-            s_i = S.soff[crow + 1] + (h - S.hoff[r]);
-            int lx = 1;
-            while (lx < bx && S.soff[crow + lx + 1] <= s_i) ++lx;
-            const int c = crow + lx;
-            pi = S.sp[s_i];
-            lo[0] = s_i + 1;
-            hi[0] = S.soff[c + 2];
-            const int c1 = (lx - 1) + sxa * (ly + 1) + rowz * lz;
-            lo[1] = S.soff[c1];
-            hi[1] = S.soff[c1 + 3];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const int c2 = (lx - 1) + sxa * (ly - 1 + d) + rowz * (lz + 1);
-                lo[2 + d] = S.soff[c2];
-                hi[2 + d] = S.soff[c2 + 3];
-            }
-        }
-#pragma unroll
+    for (int h = tid; h < nhome; h += FT_NTHR) {
+        int r = 0;
+        while (r + 1 < by * bz && S.hoff[r + 1] <= h) ++r;
+        const int lz = r >= by ? 1 : 0;
+        const int ly = 1 + r - lz * by;
+        const int crow = sxa * (ly + sya * lz);
+        const int s_i = S.soff[crow + 1] + (h - S.hoff[r]);
+        int lx = 1;
+        while (lx < bx && S.soff[crow + lx + 1] <= s_i) ++lx;
+        const int c = crow + lx;
+        const int c1 = c - 1 + sxa; // (lx - 1, ly + 1, lz): the y+1 row
+        const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
+        const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[h * FT_LSTRIDE]);
+        unsigned lptr = lbase;
+        bool full = false;
+#pragma unroll 1
         for (int k = 0; k < 5; ++k) {
-            int a = lo[k];
-            const int b = hi[k];
-            // chunks of at most FT_LCAP candidates; evaluate the lists early if they could
-            // overflow (rare at rho = 8: a segment holds ~24 candidates)
-            while (__any_sync(0xffffffffu, a < b)) {
-                const int e = min(b, a + FT_LCAP);
-                if (__any_sync(0xffffffffu, cnt + (e - a) > FT_LCAP)) {
-                    __syncwarp();
-                    tile_pairs<RECORD, KMODE>(S, lane, tid, cnt, s_i, pp, fx, ks, rec, err);
-                    cnt = 0;
-                    __syncwarp();
+            // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
+            const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
+            int a = (k == 0) ? s_i + 1 : S.soff[cs];
+            const int b = S.soff[cs + (k == 0 ? 2 : 3)];
+            // a chunk of m candidates adds at most m entries: sweep in chunks that fit the
+            // remaining list capacity; once the list is full (first particle of a crowded
+            // cell, ~4 sigma) the remaining candidates are evaluated in place
+            while (a < b) {
+                const int room = FT_LCAP - (int)((lptr - lbase) >> 1);
+                if (room <= 0) {
+                    full = true;
+                    break;
                 }
-                unsigned lptr = lbase + 2u * (unsigned)cnt;
-                sweep(S, lptr, a, e, pi.x, pi.y, pi.z, pp.rc2);
-                cnt = (int)(lptr - lbase) >> 1;
+                const int e = min(b, a + room);
+                sweep(S, lptr, a, e, px, py, pz, pp.rc2);
                 a = e;
             }
+            if (full) {
+                const float4 pi = S.sp[s_i], vi = S.sv[s_i];
+                for (; a < b; ++a) {
+                    if (!(r2_one(S, a, px, py, pz) < pp.rc2)) continue;
+                    float dx, dy, dz;
+                    const float s = pair_eval<RECORD, KMODE>(pp, fx, pi, vi, S.sp[a], S.sv[a], ks, rec, err, dx, dy, dz);
+                    const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
+                              qz = to_fixed(s * dz, fx.scale);
+                    atomicAdd(&S.acc[0][s_i], qx);
+                    atomicAdd(&S.acc[1][s_i], qy);
+                    atomicAdd(&S.acc[2][s_i], qz);
+                    atomicAdd(&S.acc[0][a], -qx);
+                    atomicAdd(&S.acc[1][a], -qy);
+                    atomicAdd(&S.acc[2][a], -qz);
+                }
+            }
         }
-        __syncwarp();
-        tile_pairs<RECORD, KMODE>(S, lane, tid, cnt, s_i, pp, fx, ks, rec, err);
-        __syncwarp();
+        if (full && tid == h) atomicAdd(&err[6], 1); // statistics: in-place evaluations
+        S.hcnt[h] = (int)(lptr - lbase) >> 1;
+        S.hsi[h] = s_i;
+    }
+    __syncthreads();
+
+    // ---- 3. compacted owner table and CTA-wide prefix over the list lengths -------------
+    // thread t handles home particles t and t + FT_NTHR (nhome <= FT_HCAP < 2 FT_NTHR)
+    const int h0 = tid, h1 = tid + FT_NTHR;
+    const int n0 = h0 < nhome ? S.hcnt[h0] : 0, n1 = h1 < nhome ? S.hcnt[h1] : 0;
+    const int k0 = n0 > 0, k1 = n1 > 0;
+    int pexcl = 0, oexcl = 0;
+    // two scans packed into one: low 16 bits = owners, high 16 bits = entries
+    const int packed_tot = block_excl_scan(S, (k0 + k1) | ((n0 + n1) << 16), pexcl, lane, warp);
+    oexcl = pexcl & 0xFFFF;
+    int eexcl = pexcl >> 16;
+    if (k0) {
+        S.oexcl[oexcl] = eexcl;
+        S.osi[oexcl] = S.hsi[h0];
+        S.orow[oexcl] = h0 * FT_LSTRIDE - eexcl;
+        ++oexcl;
+        eexcl += n0;
+    }
+    if (k1) {
+        S.oexcl[oexcl] = eexcl;
+        S.osi[oexcl] = S.hsi[h1];
+        S.orow[oexcl] = h1 * FT_LSTRIDE - eexcl;
+    }
+    const int nown = packed_tot & 0xFFFF;
+    const int tot = packed_tot >> 16;
+    if (tid == 0) S.oexcl[nown] = tot;
+    __syncthreads();
+
+    // ---- 4. pair evaluation: contiguous chunk of the CTA-wide list per thread, walked by
+    //         two independent cursors (halves of the chunk) so two Philox/Box-Muller chains
+    //         are in flight per thread (instruction-level parallelism at 2 CTAs / SM)
+    {
+        const int C = (tot + FT_NTHR - 1) / FT_NTHR;
+        const int t0 = min(tid * C, tot);
+        const int t1 = min(t0 + C, tot);
+        const int tm = t0 + ((t1 - t0 + 1) >> 1);
+        PairCursor A, B;
+        cursor_init(A, S, t0, tm, nown);
+        cursor_init(B, S, tm, t1, nown);
+        while (A.t < A.t1) { // B is never longer than A
+            const int ja = cursor_next(A, S);
+            const bool bact = B.t < B.t1;
+            const int jb = bact ? cursor_next(B, S) : B.si; // inactive: self pair, r2 = 0 -> f = 0
+            float dxa, dya, dza, dxb, dyb, dzb;
+            const float sa = pair_core<KMODE>(pp, A.pi, A.vi, S.sp[ja], S.sv[ja], ks, dxa, dya, dza);
+            const float sb = pair_core<KMODE>(pp, B.pi, B.vi, S.sp[jb], S.sv[jb], ks, dxb, dyb, dzb);
+            pair_checks<RECORD>(pp, fx, A.pi, S.sp[ja], sa, dxa, dya, dza, ks, rec, err);
+            if (bact) pair_checks<RECORD>(pp, fx, B.pi, S.sp[jb], sb, dxb, dyb, dzb, ks, rec, err);
+            cursor_accumulate(A, S, ja, sa, dxa, dya, dza, fx.scale);
+            if (bact) cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale);
+        }
+        cursor_flush(A, S);
+        cursor_flush(B, S);
     }
     __syncthreads();
 
     // ---- 5. flush: fixed point -> fp32, one vector reduction per staged particle -------
-    for (int s = tid; s < total; s += FT_NTHR) {
-        const int qx = S.acc[0][s], qy = S.acc[1][s], qz = S.acc[2][s];
-        if (qx | qy | qz)
-            atomicAdd(&frc[S.gidx[s]], make_float4((float)qx * fx.inv_scale, (float)qy * fx.inv_scale,
-                                                   (float)qz * fx.inv_scale, 0.0f));
+    // rows map back to <= 3 contiguous global segments, exactly as they were staged
+    for (int row = warp; row < sya * sza; row += FT_NWARP) {
+        const int c0 = sxa * row;
+        const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
+        const bool wrap_lo = (x0 == 0), wrap_hi = (x0 + bx == g.n[0]);
+        const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
+        const int gm = wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0];
+        for (int s = a0 + lane; s < e0; s += 32) {
+            const int gi = (s < mlo) ? S.cgs[c0] + (s - a0)
+                                     : (s < mhi ? gm + (s - mlo) : S.cgs[c0 + bx + 1] + (s - c0s));
+            const int qx = S.acc[0][s], qy = S.acc[1][s], qz = S.acc[2][s];
+            if (qx | qy | qz)
+                atomicAdd(&frc[gi], make_float4((float)qx * fx.inv_scale, (float)qy * fx.inv_scale,
+                                                (float)qz * fx.inv_scale, 0.0f));
+        }
     }
 }
 

@@ -193,6 +193,23 @@ def test_per_step_parity_config1(kernel):
     print(f"worst relative force error {worst:.2e}")
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_dense_cluster_overflow_fallback(kernel):
+    """A dense blob (rho ~ 60 locally) overflows the tiled kernel's shared-memory tiles; the
+    global-memory fallback must give the same forces (and the reference kernel too)."""
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    rng = np.random.default_rng(4)
+    blob = (rng.random((1500, 3)) * 3.0 + 2.0).astype(np.float32)   # 3^3 volume: rho ~ 56
+    fluid = (rng.random((600, 3)) * 8.0).astype(np.float32)
+    pos = np.concatenate([blob, fluid])
+    vel = rng.normal(size=pos.shape).astype(np.float32)
+    d = _ctx(cfg, kernel=kernel)
+    d.set_particles(pos, vel)
+    F_ref, allow, _ = oracle.forces(p, pos, vel, 0, eps=boundary_eps(cfg.box))
+    check_forces(d.get_forces(), F_ref, allow)
+
+
 def test_momentum_and_force_sum():
     cfg = workloads.CONFIGS["parity"]
     pos0, vel0 = workloads.make_config(cfg)
