@@ -161,6 +161,14 @@ int dpd_get_launch_count(const dpd_ctx *ctx, int64_t *launches);
 
 /* ---- multi-GPU (3D domain decomposition) ---------------------------------- */
 
+/* Communication plan of one rank (host only, no GPU needed): for each direction index
+ * d = (dx+1) + 3 (dy+1) + 9 (dz+1), the rank its message goes to (coord + D, periodic),
+ * the rank it receives direction-d messages from (coord - D), and whether d is used (every
+ * nonzero component lies in a split dimension, grid > 1).  Messages are posted in
+ * increasing d on every rank, which makes point-to-point matching order-consistent. */
+int dpd_plan_peers(const int32_t grid[3], int rank, int32_t peer_to[27], int32_t peer_from[27],
+                   int32_t used[27]);
+
 /* Write a fresh NCCL unique id (128 bytes) for rank 0 to broadcast to the others. */
 int dpd_nccl_unique_id(uint8_t id[128]);
 

@@ -56,6 +56,7 @@ SIGNATURES = [
     ("dpd_get_timing", C.c_int, [_vp, C.c_int, _P(C.c_double), _P(C.c_int64)]),
     ("dpd_kernel_name", C.c_char_p, [C.c_int]),
     ("dpd_get_launch_count", C.c_int, [_vp, _P(C.c_int64)]),
+    ("dpd_plan_peers", C.c_int, [_P(C.c_int32), C.c_int, _vp, _vp, _vp]),
     ("dpd_nccl_unique_id", C.c_int, [_vp]),
     ("dpd_create_dist", C.c_int, [_P(C.c_double), C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_uint64, C.c_int, C.c_int, _P(C.c_int32), _vp, _P(_vp)]),
@@ -163,6 +164,8 @@ def dpd_sync(ctx):
 
 
 def dpd_get_count(ctx):
+    """Current local count (synchronises first: migration changes it on the device)."""
+    _check(ctx, load().dpd_sync(ctx))
     n = C.c_int64()
     _check(ctx, load().dpd_get_count(ctx, C.byref(n)))
     return n.value
@@ -355,3 +358,15 @@ def dpd_get_forces_ex(ctx, f=None, ids=None):
     cnt = C.c_int64()
     _check(ctx, load().dpd_get_forces_ex(ctx, int(f.shape[0]), _ptr(f), _ptr(ids), C.byref(cnt)))
     return f[: cnt.value], ids[: cnt.value]
+
+
+def dpd_plan_peers(grid, rank):
+    """(peer_to[27], peer_from[27], used[27]) of `rank` on the rank grid (host only)."""
+    g = (C.c_int32 * 3)(*[int(x) for x in grid])
+    to = np.zeros(27, np.int32)
+    fr = np.zeros(27, np.int32)
+    us = np.zeros(27, np.int32)
+    code = load().dpd_plan_peers(g, int(rank), _ptr(to), _ptr(fr), _ptr(us))
+    if code != DPD_OK:
+        raise DPDError(code, "dpd_plan_peers")
+    return to, fr, us.astype(bool)

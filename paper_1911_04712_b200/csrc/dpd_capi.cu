@@ -1,8 +1,21 @@
-// dpd_capi.cu -- C-ABI (include/dpd.h) and the per-context step engine.
+// dpd_capi.cu -- C-ABI (include/dpd.h) and the per-(sub)domain step engine.
 //
-// The engine owns all device memory of one (sub)domain, launches every kernel of the
-// step on one CUDA stream, and reports device-side errors through a small error word that
-// is read back once per synchronising call (no per-step host sync).  See DESIGN.md §5-§6.
+// The engine owns all device memory of one (sub)domain, launches every kernel of the step
+// on one CUDA stream (plus a communication stream in multi-GPU runs), and reports
+// device-side errors through a small error word that is read back once per synchronising
+// call (no per-step host sync).  Particle counts live on the device (the last entry of the
+// cell-start array), so migration never needs a host round trip.  See DESIGN.md §5-§7.
+//
+// One step (GW velocity Verlet, C-6):
+//   a1-a2  k_bin          kick + drift + wrap, cell histogram; leavers -> migration messages
+//   a10    exchange(mig)  NCCL send/recv (or device copies inside an in-process group)
+//          k_bin_recv     received migrants -> histogram
+//   a3     k_scan         exclusive scan of the counts
+//   a4     k_scatter (+ k_scatter_recv)  cell-sorted copy
+//   a7     k_ghost_pack   boundary-layer particles -> ghost messages
+//   a8     exchange(ghost) on the comm stream, overlapped with
+//   a5     k_force_tile   local-local half-stencil pairs
+//   a9     k_ghost_bin/scan/scatter + k_force_halo   one-sided local-ghost pairs
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,7 +26,12 @@
 #include <string>
 #include <vector>
 
+#ifdef DPD_HAVE_NCCL
+#include <nccl.h>
+#endif
+
 #include "../../include/dpd.h"
+#include "dpd_dist.cuh"
 #include "dpd_force_tile.cuh"
 #include "dpd_kernels.cuh"
 
@@ -29,9 +47,14 @@ enum KernelId {
     KID_FORCE,
     KID_GATHER,
     KID_DEBUG,
+    KID_MIGRATE,
+    KID_GHOST_PACK,
+    KID_GHOST_SORT,
+    KID_HALO,
     KID_COUNT
 };
-const char *kKernelNames[KID_COUNT] = {"pack", "bin", "scan", "scatter", "force", "gather", "debug"};
+const char *kKernelNames[KID_COUNT] = {"pack",    "bin",        "scan",       "scatter", "force", "gather",
+                                       "debug",   "migrate",    "ghost_pack", "ghost_sort", "halo"};
 
 template <class T>
 struct DevBuf {
@@ -61,11 +84,20 @@ struct PendingTiming {
     int kid;
 };
 
+// Message area of one kind (ghosts or migrants): 27 direction slots, see Msgs.
+struct MsgArea {
+    DevBuf<char> send, recv;
+    Msgs ms{}, mr{}; // device views of send / recv
+    size_t bytes[27] = {0};
+    int maxcap = 0;
+};
+
 } // namespace
 
 struct dpd_ctx {
     // parameters
-    double box[3];
+    double box[3];   // global box
+    double sub[3];   // subdomain extent
     double rc, a, gamma, kT, power, dt;
     uint64_t seed;
     double body_f = 0.0;
@@ -75,19 +107,40 @@ struct dpd_ctx {
     PairP pp{};
     FixP fix{};
     float origin[3] = {0, 0, 0};
+    // decomposition
+    bool dist = false;
+    int rank = 0, world = 1, grid[3] = {1, 1, 1}, coord[3] = {0, 0, 0};
+    int peer_to[27], peer_from[27]; // rank at coord + D / coord - D (periodic), -1 if unused
+    MsgArea mig, gh;
+    double cap_factor = 1.0;
+    bool msgs_ready = false;
+    DevBuf<int> rank_in, gcount, gstart, grank;
+    DevBuf<float4> gpos, gvel;
+    DevBuf<unsigned long long> gscan_state;
+    int64_t gcap = 0;
+#ifdef DPD_HAVE_NCCL
+    ncclComm_t nccl = nullptr;
+#endif
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_ghost = nullptr;
+    dpd_ctx **group = nullptr; // in-process group (device-copy transport), shared by members
+    int group_n = 0;
     // state
-    int64_t n = 0;
+    int64_t n = 0;     // local particle count as of the last synchronisation
+    int64_t n_cap = 0; // capacity of the particle arrays
     int64_t step = 0;
-    bool primed = false; // after set: next kick is dt/2
+    bool primed = false;     // after set: next kick is dt/2
+    bool need_prime = false; // in-process group: forces not yet computed after set
     bool dense_ids = false;
-    int cur = 0; // which of the double buffers holds the current state
+    int cur = 0;  // which of the double buffers holds the current particles
+    int scur = 0; // which start array describes them (start[scur][ncell] = count)
     DevBuf<float4> pos[2], vel[2], frc[2];
-    DevBuf<int> rank, count, start;
+    DevBuf<int> rank_buf, count, start[2];
     DevBuf<unsigned long long> scan_state;
     DevBuf<unsigned> scan_epoch;
     DevBuf<int> err;
     DevBuf<float> stage;
-    int *h_err = nullptr; // pinned
+    int *h_err = nullptr; // pinned: [0..7] error word, [8] local count
     // execution
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -97,7 +150,7 @@ struct dpd_ctx {
     double t_ms[KID_COUNT] = {0};
     int64_t t_launches[KID_COUNT] = {0};
     int64_t launches = 0;
-    int64_t fallback[3] = {0, 0, 0}; // tiled-kernel fallbacks: staged / home / list capacity
+    int64_t fallback[3] = {0, 0, 0}; // tiled kernel: staged / home capacity tiles, full-list particles
     std::string last_error;
 };
 
@@ -122,6 +175,21 @@ int fail(dpd_ctx *c, int code, const char *fmt, ...)
         if (e_ != cudaSuccess)                                                                       \
             return fail((c), DPD_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
                         __FILE__, __LINE__);                                                         \
+    } while (0)
+
+#ifdef DPD_HAVE_NCCL
+#define NCCL_TRY(c, expr)                                                                            \
+    do {                                                                                             \
+        ncclResult_t r_ = (expr);                                                                    \
+        if (r_ != ncclSuccess)                                                                       \
+            return fail((c), DPD_ERR_COMM, "%s failed: %s", #expr, ncclGetErrorString(r_));          \
+    } while (0)
+#endif
+
+#define TRY(x)                      \
+    do {                            \
+        int r_ = (x);               \
+        if (r_ != DPD_OK) return r_; \
     } while (0)
 
 cudaEvent_t get_event(dpd_ctx *c)
@@ -158,12 +226,6 @@ int launch(dpd_ctx *c, int kid, F &&f)
     return DPD_OK;
 }
 
-#define TRY(x)                      \
-    do {                            \
-        int r_ = (x);               \
-        if (r_ != DPD_OK) return r_; \
-    } while (0)
-
 int resolve_timing(dpd_ctx *c)
 {
     for (auto &p : c->pending) {
@@ -178,12 +240,16 @@ int resolve_timing(dpd_ctx *c)
     return DPD_OK;
 }
 
-// Synchronise and translate the device error word.
+inline int *count_ptr(dpd_ctx *c) { return c->start[c->scur].p + c->geom.ncell; }
+
+// Synchronise, read the local count and translate the device error word.
 int sync_check(dpd_ctx *c)
 {
     CUDA_TRY(c, cudaMemcpyAsync(c->h_err, c->err.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_err + 8, count_ptr(c), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     resolve_timing(c);
+    c->n = c->h_err[8];
     if (c->h_err[4] | c->h_err[5] | c->h_err[6]) {
         for (int k = 0; k < 3; ++k) c->fallback[k] += c->h_err[4 + k];
         CUDA_TRY(c, cudaMemsetAsync(c->err.p + 4, 0, 4 * sizeof(int), c->stream));
@@ -196,9 +262,12 @@ int sync_check(dpd_ctx *c)
         if (flags & ERR_NONFINITE)
             return fail(c, DPD_ERR_NUMERIC, "non-finite value (particle id %d) at step <= %lld", id,
                         (long long)c->step);
-        if (flags & ERR_CAPACITY) return fail(c, DPD_ERR_CAPACITY, "device buffer capacity exceeded");
+        if (flags & ERR_CAPACITY)
+            return fail(c, DPD_ERR_CAPACITY, "device buffer capacity exceeded (particles, ghosts or migrants)");
         if (flags & ERR_RANGE)
-            return fail(c, DPD_ERR_NUMERIC, "particle id %d moved more than one box length in a step", id);
+            return fail(c, DPD_ERR_NUMERIC,
+                        "particle id %d moved more than one (sub)domain in a step or a pair force left the "
+                        "fixed-point range", id);
         return fail(c, DPD_ERR_NUMERIC, "device error flags 0x%x", flags);
     }
     return DPD_OK;
@@ -214,7 +283,8 @@ int ensure_capacity(dpd_ctx *c, int64_t n)
         CUDA_TRY(c, c->vel[b].reserve(want));
         CUDA_TRY(c, c->frc[b].reserve(want));
     }
-    CUDA_TRY(c, c->rank.reserve(want));
+    CUDA_TRY(c, c->rank_buf.reserve(want));
+    c->n_cap = (int64_t)c->pos[0].cap;
     return DPD_OK;
 }
 
@@ -228,52 +298,98 @@ IntegP integ(const dpd_ctx *c, float dt_drift, float kick)
     return ip;
 }
 
-// Cell-list build of the current buffers into the other buffer set (a1-a4); flips cur.
-int rebuild(dpd_ctx *c, const IntegP &ip)
+Msgs no_msgs()
 {
-    const int n = (int)c->n;
-    const int s = c->cur, d = 1 - c->cur;
+    Msgs m{};
+    m.base = nullptr;
+    return m;
+}
+
+// ---- phases of one step -------------------------------------------------------------------
+
+// a1-a2: kick-drift and histogram (leavers into the migration messages).  with_mig = false
+// when re-binning a freshly set state (dt = 0: nobody moves, no messages).
+int phase_bin(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
+{
     const Geom g = c->geom;
-    if (n > 0) {
-        TRY(launch(c, KID_BIN, [&] {
-            k_bin<<<nblk(n, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p, n, g, ip, c->count.p,
-                                                      c->rank.p, c->err.p);
+    const int s = c->cur;
+    with_mig = with_mig && c->dist;
+    const Msgs mig = with_mig ? c->mig.ms : no_msgs();
+    if (with_mig) {
+        TRY(launch(c, KID_MIGRATE, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(mig); }));
+    }
+    return launch(c, KID_BIN, [&] {
+        k_bin<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p, count_ptr(c), g, ip,
+                                                         c->count.p, c->rank_buf.p, mig, c->err.p);
+    });
+}
+
+// a10 (received side) + a3 + a4: histogram of the migrants, scan, scatter; flips cur/scur.
+int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
+{
+    const Geom g = c->geom;
+    const int s = c->cur, d = 1 - c->cur;
+    const int ss = c->scur, sd = 1 - c->scur;
+    with_mig = with_mig && c->dist;
+    if (with_mig) {
+        const dim3 grid(nblk(c->mig.maxcap, 256), 27);
+        const Msgs mr = c->mig.mr;
+        TRY(launch(c, KID_MIGRATE, [&] {
+            k_bin_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->count.p, c->rank_in.p, c->err.p);
         }));
     }
     const int ntile = (g.ncell + kScanTile - 1) / kScanTile;
     TRY(launch(c, KID_SCAN, [&] {
-        k_scan<<<ntile, kScanThreads, 0, c->stream>>>(c->count.p, c->start.p, g.ncell, c->scan_state.p,
+        k_scan<<<ntile, kScanThreads, 0, c->stream>>>(c->count.p, c->start[sd].p, g.ncell, c->scan_state.p,
                                                       c->scan_epoch.p);
     }));
-    if (n > 0) {
-        TRY(launch(c, KID_SCATTER, [&] {
-            k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p, n, g, ip,
-                                                          c->start.p, c->rank.p, c->pos[d].p, c->vel[d].p,
-                                                          c->frc[d].p);
+    TRY(launch(c, KID_SCATTER, [&] {
+        k_scatter<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p,
+                                                              c->start[ss].p + g.ncell, g, ip, c->start[sd].p,
+                                                              c->rank_buf.p, c->pos[d].p, c->vel[d].p, c->frc[d].p);
+    }));
+    if (with_mig) {
+        const dim3 grid(nblk(c->mig.maxcap, 256), 27);
+        const Msgs mr = c->mig.mr;
+        TRY(launch(c, KID_MIGRATE, [&] {
+            k_scatter_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->start[sd].p, c->rank_in.p,
+                                                        c->pos[d].p, c->vel[d].p, c->frc[d].p);
         }));
     }
     c->cur = d;
+    c->scur = sd;
     return DPD_OK;
 }
 
-// Force pass on the current buffers at RNG step index `step` (a5).
+// a7: boundary layers -> ghost messages.
+int phase_ghost_pack(dpd_ctx *c)
+{
+    const Geom g = c->geom;
+    const Msgs gs = c->gh.ms;
+    TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(gs); }));
+    return launch(c, KID_GHOST_PACK, [&] {
+        k_ghost_pack<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[c->cur].p, c->vel[c->cur].p, count_ptr(c), g,
+                                                                 gs, c->err.p);
+    });
+}
+
+// a5: local-local pairs at RNG step index `step`.
 int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool record)
 {
-    const int n = (int)c->n;
-    if (n == 0) return DPD_OK;
     const int b = c->cur;
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const Geom g = c->geom;
     const PairP pp = c->pp;
-    if (c->force_impl == 0) {
+    if (c->force_impl == 0 || c->dist) {
         const FixP fx = c->fix;
         const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
                           ((g.n[2] + FT_BZ - 1) / FT_BZ);
         const size_t smem = sizeof(ForceTileSmem);
+        const int *st = c->start[c->scur].p;
         return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
 #define DPD_TILE(R, K)                                                                                              \
-    k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, g, pp,  \
-                                                            fx, s_lo, s_hi, rec, c->err.p)
+    k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, s_lo, \
+                                                            s_hi, rec, c->err.p)
             if (record) {
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;
@@ -290,22 +406,244 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
 #undef DPD_TILE
         });
     }
+    const int n = (int)c->n;
+    if (n == 0) return DPD_OK;
+    const int *st = c->start[c->scur].p;
     return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
         const unsigned grid = nblk(n, 128);
+#define DPD_REF(R, K)                                                                                               \
+    k_force_ref<R, K><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, n, g, pp, s_lo, s_hi, rec)
         if (record) {
             switch (c->kmode) {
-            case 0: k_force_ref<true, 0><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, n, g, pp, s_lo, s_hi, rec); break;
-            case 1: k_force_ref<true, 1><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, n, g, pp, s_lo, s_hi, rec); break;
-            default: k_force_ref<true, 2><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, n, g, pp, s_lo, s_hi, rec); break;
+            case 0: DPD_REF(true, 0); break;
+            case 1: DPD_REF(true, 1); break;
+            default: DPD_REF(true, 2); break;
             }
         } else {
             switch (c->kmode) {
-            case 0: k_force_ref<false, 0><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, n, g, pp, s_lo, s_hi, rec); break;
-            case 1: k_force_ref<false, 1><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, n, g, pp, s_lo, s_hi, rec); break;
-            default: k_force_ref<false, 2><<<grid, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, c->start.p, n, g, pp, s_lo, s_hi, rec); break;
+            case 0: DPD_REF(false, 0); break;
+            case 1: DPD_REF(false, 1); break;
+            default: DPD_REF(false, 2); break;
             }
         }
+#undef DPD_REF
     });
+}
+
+// a9: received ghosts -> halo cells, then one-sided local-ghost forces.
+int phase_halo(dpd_ctx *c, int64_t step)
+{
+    const Geom g = c->geom;
+    const Msgs gr = c->gh.mr;
+    const dim3 grid(nblk(c->gh.maxcap, 256), 27);
+    TRY(launch(c, KID_GHOST_SORT, [&] {
+        k_ghost_bin<<<grid, 256, 0, c->stream>>>(gr, g, c->gh.maxcap, c->gcount.p, c->grank.p, c->err.p);
+    }));
+    const int ntile = (g.ncell + kScanTile - 1) / kScanTile;
+    TRY(launch(c, KID_GHOST_SORT, [&] {
+        k_scan<<<ntile, kScanThreads, 0, c->stream>>>(c->gcount.p, c->gstart.p, g.ncell, c->gscan_state.p,
+                                                      c->scan_epoch.p + 1);
+    }));
+    TRY(launch(c, KID_GHOST_SORT, [&] {
+        k_ghost_scatter<<<grid, 256, 0, c->stream>>>(gr, g, c->gh.maxcap, c->gstart.p, c->grank.p, c->gpos.p,
+                                                     c->gvel.p);
+    }));
+    const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
+    const PairP pp = c->pp;
+    const int b = c->cur;
+    return launch(c, KID_HALO, [&] {
+        const unsigned nb = nblk(c->n_cap, 128);
+        switch (c->kmode) {
+        case 0: k_force_halo<0><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
+        case 1: k_force_halo<1><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
+        default: k_force_halo<2><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
+        }
+    });
+}
+
+// ---- transports ---------------------------------------------------------------------------
+// Message of direction d travels from rank r to peer_to[d] and lands in that rank's receive
+// slot d.  Both ends post their sends / receives in increasing d, so NCCL matches them in
+// order even when several directions connect the same pair of ranks (2 ranks along a
+// dimension); the in-process group copies send slot d of every member to recv slot d of
+// peer_to[d].
+
+int exchange_nccl(dpd_ctx *c, MsgArea &m, cudaStream_t st)
+{
+#ifdef DPD_HAVE_NCCL
+    NCCL_TRY(c, ncclGroupStart());
+    for (int d = 0; d < 27; ++d) {
+        if (m.bytes[d] == 0) continue;
+        NCCL_TRY(c, ncclSend(m.send.p + m.ms.off[d], m.bytes[d], ncclChar, c->peer_to[d], c->nccl, st));
+        NCCL_TRY(c, ncclRecv(m.recv.p + m.mr.off[d], m.bytes[d], ncclChar, c->peer_from[d], c->nccl, st));
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+    return DPD_OK;
+#else
+    (void)m;
+    (void)st;
+    return fail(c, DPD_ERR_COMM, "libdpd was built without NCCL");
+#endif
+}
+
+int exchange_group(dpd_ctx **g, int n, bool ghosts)
+{
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        MsgArea &m = ghosts ? c->gh : c->mig;
+        for (int d = 0; d < 27; ++d) {
+            if (m.bytes[d] == 0) continue;
+            dpd_ctx *p = g[c->peer_to[d]];
+            MsgArea &pm = ghosts ? p->gh : p->mig;
+            CUDA_TRY(c, cudaMemcpyAsync(pm.recv.p + pm.mr.off[d], m.send.p + m.ms.off[d], m.bytes[d],
+                                        cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+    return DPD_OK;
+}
+
+// ---- message buffers ------------------------------------------------------------------------
+// Capacities from the global number density rho: a ghost message holds the particles of a
+// one-cell layer of its face / edge / corner, a migration message the leavers of one step
+// (|u| dt << h).  1.25 x mean + 8 sqrt(mean) + 64 keeps overflow > 8 sigma away.
+int setup_messages(dpd_ctx *c, double rho)
+{
+    const Geom &g = c->geom;
+    const double h[3] = {c->sub[0] / g.n[0], c->sub[1] / g.n[1], c->sub[2] / g.n[2]};
+    const double vmax = 4.0 * std::sqrt(std::max(c->kT, 1e-6)) + 1.0; // per-component speed bound
+    size_t goff = 0, moff = 0;
+    int gmax = 0, mmax = 0;
+    for (int d = 0; d < 27; ++d) {
+        const int D[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+        bool used = d != 13;
+        double vol_g = 1.0, vol_m = 1.0;
+        for (int k = 0; k < 3; ++k) {
+            if (D[k] != 0 && !g.split[k]) used = false;
+            vol_g *= D[k] ? h[k] : c->sub[k];
+            vol_m *= D[k] ? std::min(h[k], vmax * c->dt) : c->sub[k];
+        }
+        int capg = 0, capm = 0;
+        if (used) {
+            const double mg = rho * vol_g * c->cap_factor, mm = rho * vol_m * c->cap_factor;
+            capg = (int)std::ceil(1.25 * mg + 8.0 * std::sqrt(mg) + 64.0);
+            capm = (int)std::ceil(1.25 * mm + 8.0 * std::sqrt(mm) + 64.0);
+        }
+        c->gh.ms.cap[d] = c->gh.mr.cap[d] = capg;
+        c->mig.ms.cap[d] = c->mig.mr.cap[d] = capm;
+        c->gh.ms.off[d] = c->gh.mr.off[d] = (int)goff;
+        c->mig.ms.off[d] = c->mig.mr.off[d] = (int)moff;
+        c->gh.bytes[d] = capg ? 16 + 32 * (size_t)capg : 0;
+        c->mig.bytes[d] = capm ? 16 + 32 * (size_t)capm : 0;
+        goff += c->gh.bytes[d];
+        moff += c->mig.bytes[d];
+        gmax = std::max(gmax, capg);
+        mmax = std::max(mmax, capm);
+    }
+    if (goff > ((size_t)1 << 31) || moff > ((size_t)1 << 31))
+        return fail(c, DPD_ERR_CONFIG, "message buffers too large");
+    c->gh.maxcap = gmax;
+    c->mig.maxcap = mmax;
+    CUDA_TRY(c, c->gh.send.reserve(goff + 16));
+    CUDA_TRY(c, c->gh.recv.reserve(goff + 16));
+    CUDA_TRY(c, c->mig.send.reserve(moff + 16));
+    CUDA_TRY(c, c->mig.recv.reserve(moff + 16));
+    CUDA_TRY(c, cudaMemset(c->gh.send.p, 0, goff + 16));
+    CUDA_TRY(c, cudaMemset(c->gh.recv.p, 0, goff + 16));
+    CUDA_TRY(c, cudaMemset(c->mig.send.p, 0, moff + 16));
+    CUDA_TRY(c, cudaMemset(c->mig.recv.p, 0, moff + 16));
+    c->gh.ms.base = c->gh.send.p;
+    c->gh.mr.base = c->gh.recv.p;
+    c->mig.ms.base = c->mig.send.p;
+    c->mig.mr.base = c->mig.recv.p;
+    CUDA_TRY(c, c->rank_in.reserve((size_t)27 * std::max(mmax, 1)));
+    CUDA_TRY(c, c->grank.reserve((size_t)27 * std::max(gmax, 1)));
+    int64_t gtot = 0;
+    for (int d = 0; d < 27; ++d) gtot += c->gh.ms.cap[d];
+    c->gcap = gtot;
+    CUDA_TRY(c, c->gpos.reserve((size_t)std::max<int64_t>(gtot, 1)));
+    CUDA_TRY(c, c->gvel.reserve((size_t)std::max<int64_t>(gtot, 1)));
+    c->msgs_ready = true;
+    return DPD_OK;
+}
+
+// ---- one step of one context (NCCL or single) -------------------------------------------
+int step_one(dpd_ctx *c)
+{
+    const float kick = c->primed ? (float)(0.5 * c->dt) : (float)c->dt;
+    const IntegP ip = integ(c, (float)c->dt, kick);
+    TRY(phase_bin(c, ip));
+    if (c->dist) TRY(exchange_nccl(c, c->mig, c->stream));
+    TRY(phase_sort(c, ip));
+    c->step += 1;
+    if (c->dist) {
+        TRY(phase_ghost_pack(c));
+        CUDA_TRY(c, cudaEventRecord(c->ev_pack, c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
+        TRY(exchange_nccl(c, c->gh, c->comm_stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev_ghost, c->comm_stream));
+    }
+    TRY(force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false));
+    if (c->dist) {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_ghost, 0));
+        TRY(phase_halo(c, c->step));
+    }
+    c->primed = false;
+    return DPD_OK;
+}
+
+// Forces of the freshly set state at s = step (prime, C-2 item 2), NCCL or single.
+int prime_one(dpd_ctx *c)
+{
+    if (c->dist) {
+        TRY(phase_ghost_pack(c));
+        TRY(exchange_nccl(c, c->gh, c->stream));
+    }
+    TRY(force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false));
+    if (c->dist) TRY(phase_halo(c, c->step));
+    return DPD_OK;
+}
+
+// In-process group: every phase for every member, then the device-copy exchange.
+int group_prime(dpd_ctx **g, int n)
+{
+    // identical message layouts on every member, sized from the global density
+    int64_t nglob = 0;
+    for (int r = 0; r < n; ++r) nglob += g[r]->n;
+    const double rho = (double)nglob / (g[0]->box[0] * g[0]->box[1] * g[0]->box[2]);
+    for (int r = 0; r < n; ++r)
+        if (!g[r]->msgs_ready) TRY(setup_messages(g[r], rho));
+    for (int r = 0; r < n; ++r) TRY(phase_ghost_pack(g[r]));
+    TRY(exchange_group(g, n, true));
+    for (int r = 0; r < n; ++r) {
+        TRY(force_pass(g[r], g[r]->step, g[r]->frc[g[r]->cur].p, PairRec{nullptr, nullptr, 0}, false));
+        TRY(phase_halo(g[r], g[r]->step));
+        g[r]->need_prime = false;
+    }
+    return DPD_OK;
+}
+
+int group_step(dpd_ctx **g, int n)
+{
+    IntegP ip[64];
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        ip[r] = integ(c, (float)c->dt, c->primed ? (float)(0.5 * c->dt) : (float)c->dt);
+        TRY(phase_bin(c, ip[r]));
+    }
+    TRY(exchange_group(g, n, false));
+    for (int r = 0; r < n; ++r) {
+        TRY(phase_sort(g[r], ip[r]));
+        g[r]->step += 1;
+        TRY(phase_ghost_pack(g[r]));
+    }
+    TRY(exchange_group(g, n, true));
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        TRY(force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false));
+        TRY(phase_halo(c, c->step));
+        c->primed = false;
+    }
+    return DPD_OK;
 }
 
 int validate_params(dpd_ctx *c, const double box[3], double rc, double a, double gamma, double kT, double power,
@@ -324,7 +662,7 @@ int validate_params(dpd_ctx *c, const double box[3], double rc, double a, double
     return DPD_OK;
 }
 
-// Geometry of a (sub)domain of extent ext_len with the given split flags.
+// Geometry of a (sub)domain of extent len with the given split flags.
 int setup_geometry(dpd_ctx *c, const double len[3], const int split[3])
 {
     Geom g{};
@@ -340,6 +678,7 @@ int setup_geometry(dpd_ctx *c, const double len[3], const int split[3])
         volatile float nf = (float)nd, lf = (float)len[k];
         g.inv_h[k] = nf / lf;
         ncell *= g.ext[k];
+        c->sub[k] = len[k];
     }
     if (ncell > (int64_t)1 << 30) return fail(c, DPD_ERR_CONFIG, "too many cells (%lld)", (long long)ncell);
     g.ncell = (int)ncell;
@@ -360,6 +699,7 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     c->dt = dt;
     c->seed = seed;
     c->kmode = (power == 0.5) ? 0 : (power == 1.0 ? 1 : 2);
+    for (int d = 0; d < 27; ++d) c->peer_to[d] = c->peer_from[d] = -1;
     PairP pp;
     pp.a = (float)a;
     pp.gamma = (float)gamma;
@@ -397,9 +737,9 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     c->own_stream = true;
     CUDA_TRY(c, c->err.reserve(8));
     CUDA_TRY(c, cudaMemset(c->err.p, 0, 8 * sizeof(int)));
-    CUDA_TRY(c, cudaMallocHost(&c->h_err, 8 * sizeof(int)));
-    CUDA_TRY(c, c->scan_epoch.reserve(1));
-    CUDA_TRY(c, cudaMemset(c->scan_epoch.p, 0, sizeof(unsigned)));
+    CUDA_TRY(c, cudaMallocHost(&c->h_err, 16 * sizeof(int)));
+    CUDA_TRY(c, c->scan_epoch.reserve(2));
+    CUDA_TRY(c, cudaMemset(c->scan_epoch.p, 0, 2 * sizeof(unsigned)));
     return DPD_OK;
 }
 
@@ -407,11 +747,69 @@ int alloc_grid(dpd_ctx *c)
 {
     const int ncell = c->geom.ncell;
     CUDA_TRY(c, c->count.reserve((size_t)ncell + 16));
-    CUDA_TRY(c, c->start.reserve((size_t)ncell + 16));
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(c, c->start[b].reserve((size_t)ncell + 16));
+        CUDA_TRY(c, cudaMemset(c->start[b].p, 0, sizeof(int) * c->start[b].cap));
+    }
     const int ntile = (ncell + kScanTile - 1) / kScanTile;
     CUDA_TRY(c, c->scan_state.reserve((size_t)ntile));
     CUDA_TRY(c, cudaMemset(c->count.p, 0, sizeof(int) * c->count.cap));
     CUDA_TRY(c, cudaMemset(c->scan_state.p, 0, sizeof(unsigned long long) * c->scan_state.cap));
+    if (c->dist) {
+        CUDA_TRY(c, c->gcount.reserve((size_t)ncell + 16));
+        CUDA_TRY(c, c->gstart.reserve((size_t)ncell + 16));
+        CUDA_TRY(c, c->gscan_state.reserve((size_t)ntile));
+        CUDA_TRY(c, cudaMemset(c->gcount.p, 0, sizeof(int) * c->gcount.cap));
+        CUDA_TRY(c, cudaMemset(c->gstart.p, 0, sizeof(int) * c->gstart.cap));
+        CUDA_TRY(c, cudaMemset(c->gscan_state.p, 0, sizeof(unsigned long long) * c->gscan_state.cap));
+    }
+    return DPD_OK;
+}
+
+// Rank grid bookkeeping: coordinates and the peers of every direction.
+void setup_ranks(dpd_ctx *c, int rank, const int32_t grid[3])
+{
+    c->rank = rank;
+    for (int k = 0; k < 3; ++k) c->grid[k] = grid[k];
+    c->world = grid[0] * grid[1] * grid[2];
+    c->coord[0] = rank % grid[0];
+    c->coord[1] = (rank / grid[0]) % grid[1];
+    c->coord[2] = rank / (grid[0] * grid[1]);
+    for (int d = 0; d < 27; ++d) {
+        const int D[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+        int to[3], from[3];
+        for (int k = 0; k < 3; ++k) {
+            to[k] = (c->coord[k] + D[k] + grid[k]) % grid[k];
+            from[k] = (c->coord[k] - D[k] + grid[k]) % grid[k];
+        }
+        c->peer_to[d] = to[0] + grid[0] * (to[1] + grid[1] * to[2]);
+        c->peer_from[d] = from[0] + grid[0] * (from[1] + grid[1] * from[2]);
+    }
+    for (int k = 0; k < 3; ++k) c->origin[k] = (float)(c->coord[k] * c->sub[k]);
+}
+
+int create_common(const double box[3], double rc, double a, double gamma, double kT, double power, double dt,
+                  uint64_t seed, int rank, const int32_t grid[3], dpd_ctx **out, dpd_ctx *c)
+{
+    int r = init_ctx(c, box, rc, a, gamma, kT, power, dt, seed);
+    if (r != DPD_OK) return r;
+    double sub[3];
+    int split[3];
+    for (int k = 0; k < 3; ++k) {
+        if (grid[k] < 1) return fail(c, DPD_ERR_CONFIG, "grid[%d] = %d must be >= 1", k, grid[k]);
+        sub[k] = box[k] / grid[k];
+        split[k] = grid[k] > 1;
+    }
+    c->dist = split[0] || split[1] || split[2];
+    TRY(setup_geometry(c, sub, split));
+    setup_ranks(c, rank, grid);
+    TRY(alloc_grid(c));
+    if (c->dist) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+        CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ghost, cudaEventDisableTiming));
+    }
+    *out = c;
     return DPD_OK;
 }
 
@@ -428,47 +826,69 @@ int dpd_create(const double box[3], double rc, double a, double gamma, double kT
     if (!out || !box) return DPD_ERR_ARG;
     *out = nullptr;
     dpd_ctx *c = new dpd_ctx();
-    int r = init_ctx(c, box, rc, a, gamma, kT, power, dt, seed);
-    if (r == DPD_OK) {
-        const int split[3] = {0, 0, 0};
-        r = setup_geometry(c, box, split);
-    }
-    if (r == DPD_OK) r = alloc_grid(c);
+    const int32_t grid[3] = {1, 1, 1};
+    int r = create_common(box, rc, a, gamma, kT, power, dt, seed, 0, grid, out, c);
     if (r != DPD_OK) {
-        // keep the message reachable: hand back the context only on success
-        static thread_local std::string msg;
-        msg = c->last_error;
+        fprintf(stderr, "dpd_create: %s\n", c->last_error.c_str());
+        *out = nullptr;
         dpd_destroy(c);
-        fprintf(stderr, "dpd_create: %s\n", msg.c_str());
-        return r;
     }
-    *out = c;
-    return DPD_OK;
+    return r;
 }
 
 void dpd_destroy(dpd_ctx *c)
 {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     for (int b = 0; b < 2; ++b) {
         c->pos[b].release();
         c->vel[b].release();
         c->frc[b].release();
+        c->start[b].release();
     }
-    c->rank.release();
+    c->rank_buf.release();
     c->count.release();
-    c->start.release();
     c->scan_state.release();
     c->scan_epoch.release();
     c->err.release();
     c->stage.release();
+    c->mig.send.release();
+    c->mig.recv.release();
+    c->gh.send.release();
+    c->gh.recv.release();
+    c->rank_in.release();
+    c->gcount.release();
+    c->gstart.release();
+    c->grank.release();
+    c->gpos.release();
+    c->gvel.release();
+    c->gscan_state.release();
     for (auto &p : c->pending) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
     }
     for (auto e : c->event_pool) cudaEventDestroy(e);
+    if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+    if (c->ev_ghost) cudaEventDestroy(c->ev_ghost);
+#ifdef DPD_HAVE_NCCL
+    if (c->nccl) ncclCommDestroy(c->nccl);
+#endif
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->h_err) cudaFreeHost(c->h_err);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->group) {
+        // the group array and stream are shared: the last member to go frees them
+        int alive = 0;
+        for (int r = 0; r < c->group_n; ++r)
+            if (c->group[r] && c->group[r] != c) ++alive;
+        for (int r = 0; r < c->group_n; ++r)
+            if (c->group[r] == c) c->group[r] = nullptr;
+        if (alive == 0) {
+            delete[] c->group;
+            if (c->stream) cudaStreamDestroy(c->stream);
+        }
+    }
     delete c;
 }
 
@@ -494,7 +914,14 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
     if (!c || !name) return DPD_ERR_ARG;
     if (strcmp(name, "force_kernel") == 0) {
         if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled) or 1 (reference)");
+        if (value == 1 && c->dist) return fail(c, DPD_ERR_ARG, "the reference kernel is single-domain only");
         c->force_impl = (int)value;
+        return DPD_OK;
+    }
+    if (strcmp(name, "message_capacity_percent") == 0) {
+        if (value < 10 || value > 100000) return fail(c, DPD_ERR_ARG, "message_capacity_percent out of range");
+        c->cap_factor = value / 100.0;
+        c->msgs_ready = false; // re-sized at the next set_particles
         return DPD_OK;
     }
     return fail(c, DPD_ERR_ARG, "unknown option '%s'", name);
@@ -505,12 +932,12 @@ int dpd_get_stat(dpd_ctx *c, const char *name, int64_t *value)
     if (!c || !name || !value) return DPD_ERR_ARG;
     TRY(sync_check(c));
     if (strcmp(name, "fallback_tiles") == 0) {
-        *value = c->fallback[0] + c->fallback[1] + c->fallback[2];
+        *value = c->fallback[0] + c->fallback[1];
         return DPD_OK;
     }
     if (strcmp(name, "fallback_staged") == 0) { *value = c->fallback[0]; return DPD_OK; }
     if (strcmp(name, "fallback_home") == 0) { *value = c->fallback[1]; return DPD_OK; }
-    if (strcmp(name, "fallback_list") == 0) { *value = c->fallback[2]; return DPD_OK; }
+    if (strcmp(name, "full_list_particles") == 0) { *value = c->fallback[2]; return DPD_OK; }
     return fail(c, DPD_ERR_ARG, "unknown statistic '%s'", name);
 }
 
@@ -528,10 +955,10 @@ int dpd_set_particles_ex(dpd_ctx *c, int64_t n, const float *pos, const float *v
     if (n < 0 || n > (int64_t)INT32_MAX / 2) return fail(c, DPD_ERR_ARG, "bad particle count %lld", (long long)n);
     if (n > 0 && (!pos || !vel)) return fail(c, DPD_ERR_ARG, "null pos/vel");
     if (step0 < 0) return fail(c, DPD_ERR_ARG, "step0 must be >= 0");
-    TRY(ensure_capacity(c, n));
+    TRY(sync_check(c));
     // dense-id check (host): ids must be a permutation of 0..n-1 for id-order getters
-    bool dense = true;
-    if (ids) {
+    bool dense = !c->dist;
+    if (ids && dense) {
         std::vector<char> seen((size_t)n, 0);
         for (int64_t i = 0; i < n; ++i) {
             const int32_t id = ids[i];
@@ -541,28 +968,76 @@ int dpd_set_particles_ex(dpd_ctx *c, int64_t n, const float *pos, const float *v
         }
     }
     c->dense_ids = dense;
-    c->n = n;
     c->step = step0;
     c->cur = 0;
-    // staging: pos3, vel3 (+ ids)
+    c->scur = 0;
     const size_t words = (size_t)std::max<int64_t>(n, 1) * 7;
     CUDA_TRY(c, c->stage.reserve(words));
     float *d_pos = c->stage.p, *d_vel = c->stage.p + 3 * (size_t)n;
     int32_t *d_ids = ids ? reinterpret_cast<int32_t *>(c->stage.p + 6 * (size_t)n) : nullptr;
+    int *n_out = count_ptr(c);
+    const float3 gbox = make_float3((float)c->box[0], (float)c->box[1], (float)c->box[2]);
+    const float3 org = make_float3(c->origin[0], c->origin[1], c->origin[2]);
+    CUDA_TRY(c, cudaMemsetAsync(n_out, 0, sizeof(int), c->stream));
     if (n > 0) {
         CUDA_TRY(c, cudaMemcpyAsync(d_pos, pos, sizeof(float) * 3 * n, cudaMemcpyDefault, c->stream));
         CUDA_TRY(c, cudaMemcpyAsync(d_vel, vel, sizeof(float) * 3 * n, cudaMemcpyDefault, c->stream));
         if (ids) CUDA_TRY(c, cudaMemcpyAsync(d_ids, ids, sizeof(int32_t) * n, cudaMemcpyDefault, c->stream));
-        const Geom g = c->geom;
+    }
+    // particle arrays: exactly n on one domain; decomposed runs count the particles inside the
+    // subdomain first and leave room for migration fluctuations
+    int64_t want = n;
+    if (c->dist && n > 0) {
+        const float3 sub = make_float3((float)c->sub[0], (float)c->sub[1], (float)c->sub[2]);
         TRY(launch(c, KID_PACK, [&] {
-            k_pack_input<<<nblk(n, 256), 256, 0, c->stream>>>(d_pos, d_vel, d_ids, n, g, c->pos[0].p, c->vel[0].p,
-                                                              c->frc[0].p, c->err.p);
+            k_count_inside<<<nblk(n, 256), 256, 0, c->stream>>>(d_pos, n, gbox, org, sub, n_out);
+        }));
+        int inside = 0;
+        CUDA_TRY(c, cudaMemcpyAsync(&inside, n_out, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        want = (int64_t)(1.1 * inside + 12.0 * std::sqrt((double)inside + 1.0) + 4096.0);
+        CUDA_TRY(c, cudaMemsetAsync(n_out, 0, sizeof(int), c->stream));
+    }
+    TRY(ensure_capacity(c, want));
+    if (n > 0) {
+        const Geom g = c->geom;
+        const int cap = (int)c->n_cap;
+        TRY(launch(c, KID_PACK, [&] {
+            k_pack_input<<<nblk(n, 256), 256, 0, c->stream>>>(d_pos, d_vel, d_ids, n, g, gbox, org, c->pos[0].p,
+                                                              c->vel[0].p, c->frc[0].p, n_out, cap, c->err.p);
         }));
     }
+    TRY(sync_check(c)); // local count (capacity errors surface here)
+    if (c->dist) {
+        int64_t nglob = c->n;
+#ifdef DPD_HAVE_NCCL
+        if (c->nccl) {
+            // global count -> density for the message capacities (collective on all ranks)
+            DevBuf<long long> t;
+            CUDA_TRY(c, t.reserve(1));
+            long long v = c->n;
+            CUDA_TRY(c, cudaMemcpy(t.p, &v, sizeof v, cudaMemcpyHostToDevice));
+            NCCL_TRY(c, ncclAllReduce(t.p, t.p, 1, ncclInt64, ncclSum, c->nccl, c->stream));
+            CUDA_TRY(c, cudaMemcpyAsync(&v, t.p, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+            t.release();
+            nglob = v;
+        }
+#endif
+        // in-process groups size their messages once every member is set (dpd_group_step)
+        if (!c->group && !c->msgs_ready)
+            TRY(setup_messages(c, (double)nglob / (c->box[0] * c->box[1] * c->box[2])));
+    }
     // sort into cells without moving (dt = 0, kick = 0), then prime F_0 at s = step0
-    TRY(rebuild(c, integ(c, 0.0f, 0.0f)));
-    TRY(force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false));
+    const IntegP ip0 = integ(c, 0.0f, 0.0f);
+    TRY(phase_bin(c, ip0, false));
+    TRY(phase_sort(c, ip0, false));
     c->primed = true;
+    if (c->group) {
+        c->need_prime = true; // forces need every member's ghosts: dpd_group_step(..., 0)
+    } else {
+        TRY(prime_one(c));
+    }
     return sync_check(c);
 }
 
@@ -575,13 +1050,8 @@ int dpd_step_async(dpd_ctx *c, int64_t nsteps)
 {
     if (!c) return DPD_ERR_ARG;
     if (nsteps < 0) return fail(c, DPD_ERR_ARG, "nsteps must be >= 0");
-    for (int64_t it = 0; it < nsteps; ++it) {
-        const float kick = c->primed ? (float)(0.5 * c->dt) : (float)c->dt;
-        TRY(rebuild(c, integ(c, (float)c->dt, kick)));
-        c->step += 1;
-        TRY(force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false));
-        c->primed = false;
-    }
+    if (c->group) return fail(c, DPD_ERR_ARG, "group members are stepped with dpd_group_step");
+    for (int64_t it = 0; it < nsteps; ++it) TRY(step_one(c));
     return DPD_OK;
 }
 
@@ -618,7 +1088,7 @@ int dpd_get_grid(const dpd_ctx *c, int32_t dims[3])
     return DPD_OK;
 }
 
-static int gather(dpd_ctx *c, int64_t n, float *pos, float *vel, float *f, int by_id)
+static int gather(dpd_ctx *c, float *pos, float *vel, float *f, int by_id)
 {
     TRY(sync_check(c));
     const int64_t cnt = c->n;
@@ -636,7 +1106,6 @@ static int gather(dpd_ctx *c, int64_t n, float *pos, float *vel, float *f, int b
         k_gather_id<<<nblk(cnt, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, (int)cnt, hk,
                                                            (float)c->body_f, x_half, org, d_pos, d_vel, d_f, by_id);
     }));
-    (void)n;
     if (pos) CUDA_TRY(c, cudaMemcpyAsync(pos, d_pos, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));
     if (vel) CUDA_TRY(c, cudaMemcpyAsync(vel, d_vel, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));
     if (f) CUDA_TRY(c, cudaMemcpyAsync(f, d_f, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));
@@ -644,20 +1113,37 @@ static int gather(dpd_ctx *c, int64_t n, float *pos, float *vel, float *f, int b
     return DPD_OK;
 }
 
+static int copy_ids(dpd_ctx *c, int32_t *ids)
+{
+    if (!ids || c->n == 0) return DPD_OK;
+    CUDA_TRY(c, c->stage.reserve((size_t)c->n));
+    int32_t *d = reinterpret_cast<int32_t *>(c->stage.p);
+    const int b = c->cur;
+    const Geom g = c->geom;
+    TRY(launch(c, KID_GATHER, [&] {
+        k_ids_cells<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->pos[b].p, (int)c->n, g, d, nullptr);
+    }));
+    CUDA_TRY(c, cudaMemcpyAsync(ids, d, sizeof(int32_t) * c->n, cudaMemcpyDefault, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return DPD_OK;
+}
+
 int dpd_get_particles(dpd_ctx *c, int64_t n, float *pos, float *vel)
 {
     if (!c) return DPD_ERR_ARG;
+    TRY(sync_check(c));
     if (n != c->n) return fail(c, DPD_ERR_ARG, "n = %lld but the context holds %lld", (long long)n, (long long)c->n);
     if (!c->dense_ids) return fail(c, DPD_ERR_ARG, "ids are not dense 0..n-1; use dpd_get_particles_ex");
-    return gather(c, n, pos, vel, nullptr, 1);
+    return gather(c, pos, vel, nullptr, 1);
 }
 
 int dpd_get_forces(dpd_ctx *c, int64_t n, float *f)
 {
     if (!c) return DPD_ERR_ARG;
+    TRY(sync_check(c));
     if (n != c->n) return fail(c, DPD_ERR_ARG, "n = %lld but the context holds %lld", (long long)n, (long long)c->n);
     if (!c->dense_ids) return fail(c, DPD_ERR_ARG, "ids are not dense 0..n-1; use dpd_get_forces_ex");
-    return gather(c, n, nullptr, nullptr, f, 1);
+    return gather(c, nullptr, nullptr, f, 1);
 }
 
 int dpd_get_state(dpd_ctx *c, int64_t cap, float *pos, float *uhalf, float *f, int32_t *ids, int64_t *n)
@@ -672,9 +1158,10 @@ int dpd_get_state(dpd_ctx *c, int64_t cap, float *pos, float *uhalf, float *f, i
     float *dp = c->stage.p, *du = dp + 3 * cnt, *df = du + 3 * cnt;
     int32_t *di = reinterpret_cast<int32_t *>(df + 3 * cnt);
     const int b = c->cur;
+    const float3 org = make_float3(c->origin[0], c->origin[1], c->origin[2]);
     TRY(launch(c, KID_GATHER, [&] {
-        k_state<<<nblk(cnt, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, (int)cnt, dp, du, df,
-                                                      di);
+        k_state<<<nblk(cnt, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, (int)cnt, org, dp, du,
+                                                      df, di);
     }));
     if (pos) CUDA_TRY(c, cudaMemcpyAsync(pos, dp, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));
     if (uhalf) CUDA_TRY(c, cudaMemcpyAsync(uhalf, du, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));
@@ -687,12 +1174,13 @@ int dpd_get_state(dpd_ctx *c, int64_t cap, float *pos, float *uhalf, float *f, i
 int dpd_debug_cells(dpd_ctx *c, int32_t *cell_of_id, int32_t *count, int32_t *start)
 {
     if (!c) return DPD_ERR_ARG;
+    if (c->dist) return fail(c, DPD_ERR_ARG, "dpd_debug_cells is single-domain only");
     TRY(sync_check(c));
     const int ncell = c->geom.ncell;
     const int64_t cnt = c->n;
     if (cell_of_id && !c->dense_ids) return fail(c, DPD_ERR_ARG, "cell_of_id needs dense ids");
     std::vector<int32_t> st((size_t)ncell + 1);
-    CUDA_TRY(c, cudaMemcpy(st.data(), c->start.p, sizeof(int32_t) * (ncell + 1), cudaMemcpyDeviceToHost));
+    CUDA_TRY(c, cudaMemcpy(st.data(), c->start[c->scur].p, sizeof(int32_t) * (ncell + 1), cudaMemcpyDeviceToHost));
     if (start) memcpy(start, st.data(), sizeof(int32_t) * (ncell + 1));
     if (count)
         for (int i = 0; i < ncell; ++i) count[i] = st[i + 1] - st[i];
@@ -713,6 +1201,7 @@ int dpd_debug_cells(dpd_ctx *c, int32_t *cell_of_id, int32_t *count, int32_t *st
 int dpd_debug_pairs(dpd_ctx *c, int64_t cap, uint32_t *quad, int64_t *npairs)
 {
     if (!c || cap < 0) return DPD_ERR_ARG;
+    if (c->dist) return fail(c, DPD_ERR_ARG, "dpd_debug_pairs is single-domain only");
     TRY(sync_check(c));
     DevBuf<uint4> q;
     DevBuf<unsigned long long> cntb;
@@ -806,34 +1295,123 @@ int dpd_debug_pair_words(int64_t n, const uint32_t *quad_in, uint64_t seed, uint
     return e == cudaSuccess ? DPD_OK : DPD_ERR_CUDA;
 }
 
-// ---- multi-GPU entry points (filled in by the decomposition layer) -----------------------
+// ---- multi-GPU -------------------------------------------------------------------------------
+int dpd_plan_peers(const int32_t grid[3], int rank, int32_t peer_to[27], int32_t peer_from[27], int32_t used[27])
+{
+    if (!grid || grid[0] < 1 || grid[1] < 1 || grid[2] < 1) return DPD_ERR_ARG;
+    const int world = grid[0] * grid[1] * grid[2];
+    if (rank < 0 || rank >= world) return DPD_ERR_ARG;
+    dpd_ctx tmp; // host-only bookkeeping, no device state touched
+    for (int k = 0; k < 3; ++k) tmp.sub[k] = 1.0;
+    setup_ranks(&tmp, rank, grid);
+    for (int d = 0; d < 27; ++d) {
+        const int D[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+        bool u = d != 13;
+        for (int k = 0; k < 3; ++k)
+            if (D[k] != 0 && grid[k] < 2) u = false;
+        if (peer_to) peer_to[d] = tmp.peer_to[d];
+        if (peer_from) peer_from[d] = tmp.peer_from[d];
+        if (used) used[d] = u;
+    }
+    return DPD_OK;
+}
+
 int dpd_nccl_unique_id(uint8_t id[128])
 {
+#ifdef DPD_HAVE_NCCL
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return DPD_ERR_COMM;
+    memcpy(id, &u, 128);
+    return DPD_OK;
+#else
     (void)id;
-    return DPD_ERR_CONFIG;
+    return DPD_ERR_COMM;
+#endif
 }
 
 int dpd_create_dist(const double box[3], double rc, double a, double gamma, double kT, double power, double dt,
                     uint64_t seed, int rank, int world, const int32_t grid[3], const uint8_t nccl_id[128],
                     dpd_ctx **out)
 {
-    (void)box; (void)rc; (void)a; (void)gamma; (void)kT; (void)power; (void)dt; (void)seed;
-    (void)rank; (void)world; (void)grid; (void)nccl_id;
-    if (out) *out = nullptr;
-    return DPD_ERR_CONFIG;
+    if (!out || !box || !grid || !nccl_id) return DPD_ERR_ARG;
+    *out = nullptr;
+    if (world != grid[0] * grid[1] * grid[2] || rank < 0 || rank >= world) return DPD_ERR_ARG;
+    dpd_ctx *c = new dpd_ctx();
+    int r = create_common(box, rc, a, gamma, kT, power, dt, seed, rank, grid, out, c);
+#ifdef DPD_HAVE_NCCL
+    if (r == DPD_OK && world > 1) {
+        ncclUniqueId u;
+        memcpy(&u, nccl_id, 128);
+        ncclResult_t nr = ncclCommInitRank(&c->nccl, world, u, rank);
+        if (nr != ncclSuccess) r = fail(c, DPD_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+    }
+#else
+    if (r == DPD_OK && world > 1) r = fail(c, DPD_ERR_COMM, "libdpd was built without NCCL");
+#endif
+    if (r != DPD_OK) {
+        fprintf(stderr, "dpd_create_dist: %s\n", c->last_error.c_str());
+        *out = nullptr;
+        dpd_destroy(c);
+    }
+    return r;
 }
 
 int dpd_create_group(const double box[3], double rc, double a, double gamma, double kT, double power, double dt,
                      uint64_t seed, const int32_t grid[3], dpd_ctx **out)
 {
-    (void)box; (void)rc; (void)a; (void)gamma; (void)kT; (void)power; (void)dt; (void)seed; (void)grid; (void)out;
-    return DPD_ERR_CONFIG;
+    if (!out || !box || !grid) return DPD_ERR_ARG;
+    const int world = grid[0] * grid[1] * grid[2];
+    if (world < 1 || world > 64) return DPD_ERR_ARG;
+    dpd_ctx **members = new dpd_ctx *[world]();
+    cudaStream_t shared = nullptr;
+    for (int r = 0; r < world; ++r) {
+        dpd_ctx *c = new dpd_ctx();
+        dpd_ctx *o = nullptr;
+        int rc_ = create_common(box, rc, a, gamma, kT, power, dt, seed, r, grid, &o, c);
+        if (rc_ == DPD_OK && r == 0) {
+            shared = c->stream;
+            c->own_stream = false; // owned by the group (freed with its last member)
+        }
+        if (rc_ == DPD_OK && r > 0) {
+            // all members run on member 0's stream so the phases order themselves
+            cudaStreamDestroy(c->stream);
+            c->stream = shared;
+            c->own_stream = false;
+        }
+        if (rc_ != DPD_OK) {
+            fprintf(stderr, "dpd_create_group: %s\n", c->last_error.c_str());
+            dpd_destroy(c);
+            for (int k = 0; k < r; ++k) {
+                members[k]->group = nullptr;
+                dpd_destroy(members[k]);
+            }
+            delete[] members;
+            return rc_;
+        }
+        members[r] = c;
+    }
+    for (int r = 0; r < world; ++r) {
+        members[r]->group = members;
+        members[r]->group_n = world;
+        out[r] = members[r];
+    }
+    return DPD_OK;
 }
 
 int dpd_group_step(dpd_ctx **ctxs, int nctx, int64_t nsteps)
 {
-    (void)ctxs; (void)nctx; (void)nsteps;
-    return DPD_ERR_CONFIG;
+    if (!ctxs || nctx < 1 || nsteps < 0) return DPD_ERR_ARG;
+    dpd_ctx **g = ctxs[0]->group;
+    if (!g || ctxs[0]->group_n != nctx) return fail(ctxs[0], DPD_ERR_ARG, "not the full group of a dpd_create_group");
+    for (int r = 0; r < nctx; ++r)
+        if (ctxs[r] != g[r]) return fail(ctxs[0], DPD_ERR_ARG, "contexts must be passed in rank order");
+    bool prime = false;
+    for (int r = 0; r < nctx; ++r) prime |= g[r]->need_prime;
+    if (prime) TRY(group_prime(g, nctx));
+    for (int64_t it = 0; it < nsteps; ++it) TRY(group_step(g, nctx));
+    for (int r = 0; r < nctx; ++r) TRY(sync_check(g[r]));
+    return DPD_OK;
 }
 
 int dpd_get_particles_ex(dpd_ctx *c, int64_t cap, float *pos, float *vel, int32_t *ids, int64_t *n)
@@ -842,18 +1420,8 @@ int dpd_get_particles_ex(dpd_ctx *c, int64_t cap, float *pos, float *vel, int32_
     TRY(sync_check(c));
     if (n) *n = c->n;
     if (cap < c->n) return fail(c, DPD_ERR_ARG, "cap %lld < count %lld", (long long)cap, (long long)c->n);
-    TRY(gather(c, c->n, pos, vel, nullptr, 0));
-    if (ids && c->n > 0) {
-        int32_t *d = reinterpret_cast<int32_t *>(c->stage.p);
-        const int b = c->cur;
-        const Geom g = c->geom;
-        TRY(launch(c, KID_GATHER, [&] {
-            k_ids_cells<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->pos[b].p, (int)c->n, g, d, nullptr);
-        }));
-        CUDA_TRY(c, cudaMemcpyAsync(ids, d, sizeof(int32_t) * c->n, cudaMemcpyDefault, c->stream));
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    }
-    return DPD_OK;
+    TRY(gather(c, pos, vel, nullptr, 0));
+    return copy_ids(c, ids);
 }
 
 int dpd_get_forces_ex(dpd_ctx *c, int64_t cap, float *f, int32_t *ids, int64_t *n)
@@ -862,18 +1430,8 @@ int dpd_get_forces_ex(dpd_ctx *c, int64_t cap, float *f, int32_t *ids, int64_t *
     TRY(sync_check(c));
     if (n) *n = c->n;
     if (cap < c->n) return fail(c, DPD_ERR_ARG, "cap %lld < count %lld", (long long)cap, (long long)c->n);
-    TRY(gather(c, c->n, nullptr, nullptr, f, 0));
-    if (ids && c->n > 0) {
-        int32_t *d = reinterpret_cast<int32_t *>(c->stage.p);
-        const int b = c->cur;
-        const Geom g = c->geom;
-        TRY(launch(c, KID_GATHER, [&] {
-            k_ids_cells<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->pos[b].p, (int)c->n, g, d, nullptr);
-        }));
-        CUDA_TRY(c, cudaMemcpyAsync(ids, d, sizeof(int32_t) * c->n, cudaMemcpyDefault, c->stream));
-        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    }
-    return DPD_OK;
+    TRY(gather(c, nullptr, nullptr, f, 0));
+    return copy_ids(c, ids);
 }
 
 } // extern "C"

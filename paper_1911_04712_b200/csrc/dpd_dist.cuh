@@ -1,0 +1,233 @@
+// dpd_dist.cuh -- kernels of the 3D domain decomposition (
+// equal rectangular subdomains, halo exchange overlapped with the local
+// forces, forces due to the received particles, redistribution of leaving particles).
+//
+// Frames: each rank works in local coordinates x - origin in [0, L_sub).  A particle sent
+// in direction D (migrant or ghost) is shifted by -D L_sub, i.e. written directly in the
+// receiver's frame.  Split dimensions carry a one-cell halo ring in the extended cell grid
+// (index 0 and n + 1); ghosts are binned there, local particles never are.
+#pragma once
+
+#include "dpd_kernels.cuh"
+
+namespace dpd {
+
+__global__ void k_zero_headers(Msgs m)
+{
+    const int d = threadIdx.x;
+    if (d < 27 && m.cap[d] > 0) *msg_count(m, d) = 0;
+}
+
+__device__ __forceinline__ int msg_received(const Msgs &m, int d, int *err)
+{
+    const int c = *msg_count(m, d);
+    if (c > m.cap[d]) {
+        raise_err(err, ERR_CAPACITY, c);
+        return m.cap[d];
+    }
+    return c;
+}
+
+// Cell coordinate of a received ghost along one dimension: halo layers map to -1 / n in
+// split dimensions (x in [-h, 0) / [L, L + h)), interior otherwise (C-8 formula).
+__device__ __forceinline__ int ghost_coord(float x, float inv_h, int n, int split)
+{
+    if (!split) return cell_coord(x, inv_h, n);
+    const int q = (int)floorf(__fmul_rn(x, inv_h));
+    return min(max(q, -1), n);
+}
+
+__device__ __forceinline__ int ghost_cell(const Geom &g, float x, float y, float z)
+{
+    const int ix = ghost_coord(x, g.inv_h[0], g.n[0], g.split[0]) + g.off[0];
+    const int iy = ghost_coord(y, g.inv_h[1], g.n[1], g.split[1]) + g.off[1];
+    const int iz = ghost_coord(z, g.inv_h[2], g.n[2], g.split[2]) + g.off[2];
+    return ix + g.ext[0] * (iy + g.ext[1] * iz);
+}
+
+// ---- row a10: received migrants -> local cell histogram ---------------------------------
+// grid = (ceil(maxcap / 256), 27): block row d handles direction d's message.
+__global__ void __launch_bounds__(256) k_bin_recv(Msgs rec, Geom g, int maxcap, int *__restrict__ count,
+                                                  int *__restrict__ rank_in, int *err)
+{
+    const int d = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (rec.cap[d] == 0 || blockIdx.x * blockDim.x >= rec.cap[d]) return; // block-uniform
+    const int cnt = msg_received(rec, d, err);
+    int c = -1;
+    if (k < cnt) {
+        const float4 p = msg_data(rec, d)[2 * k];
+        const float3 x = make_float3(p.x, p.y, p.z);
+        if (!in_local_box(g, x)) raise_err(err, ERR_RANGE, __float_as_int(p.w));
+        else c = cell_index(g, p.x, p.y, p.z);
+    }
+    const int r = warp_rank_in_cell(count, c);
+    if (k < cnt) rank_in[d * maxcap + k] = (c >= 0) ? r : -1;
+}
+
+__global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxcap, const int *__restrict__ start,
+                                                      const int *__restrict__ rank_in, float4 *__restrict__ pos_o,
+                                                      float4 *__restrict__ vel_o, float4 *__restrict__ frc_o)
+{
+    const int d = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (rec.cap[d] == 0) return;
+    const int cnt = min(*msg_count(rec, d), rec.cap[d]);
+    if (k >= cnt) return;
+    const int r = rank_in[d * maxcap + k];
+    if (r < 0) return;
+    const float4 p = msg_data(rec, d)[2 * k], v = msg_data(rec, d)[2 * k + 1];
+    const int dst = start[cell_index(g, p.x, p.y, p.z)] + r;
+    pos_o[dst] = p;
+    vel_o[dst] = v;
+    frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+}
+
+// ---- row a7: ghost identify + pack ------------------------------------------------------
+// A particle in the first (last) interior cell layer of a split dimension goes to the
+// neighbour below (above); edge and corner cells go to every combination (up to 7 messages).
+__global__ void __launch_bounds__(256) k_ghost_pack(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                                                    const int *__restrict__ n_ptr, Geom g, Msgs gs, int *err)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = *n_ptr;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f), v = p;
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    if (i < n) {
+        p = pos[i];
+        v = vel[i];
+        const float xs[3] = {p.x, p.y, p.z};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (!g.split[k]) continue;
+            const int ic = cell_coord(xs[k], g.inv_h[k], g.n[k]);
+            lo[k] = ic == 0;
+            hi[k] = ic == g.n[k] - 1;
+        }
+    }
+    const int lane = threadIdx.x & 31;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int d = dir_index(dx, dy, dz);
+                if (d == 13 || gs.cap[d] == 0) continue; // uniform
+                const bool want = i < n && (dx == 0 || (dx < 0 ? lo[0] : hi[0])) &&
+                                  (dy == 0 || (dy < 0 ? lo[1] : hi[1])) && (dz == 0 || (dz < 0 ? lo[2] : hi[2]));
+                const unsigned m = __ballot_sync(0xffffffffu, want);
+                if (!m) continue;
+                int base = 0;
+                const int leader = __ffs(m) - 1;
+                if (lane == leader) base = atomicAdd(msg_count(gs, d), __popc(m));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (want) {
+                    const int slot = base + __popc(m & lanemask_lt());
+                    if (slot < gs.cap[d]) {
+                        float4 *q = msg_data(gs, d) + 2 * slot;
+                        q[0] = make_float4(p.x - dx * g.L[0], p.y - dy * g.L[1], p.z - dz * g.L[2], p.w);
+                        q[1] = v;
+                    } else {
+                        raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
+                    }
+                }
+            }
+}
+
+// ---- rows a8/a9: received ghosts -> halo cells (count, scan, scatter) ------------------
+__global__ void __launch_bounds__(256) k_ghost_bin(Msgs rec, Geom g, int maxcap, int *__restrict__ gcount,
+                                                   int *__restrict__ grank, int *err)
+{
+    const int d = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (rec.cap[d] == 0 || blockIdx.x * blockDim.x >= rec.cap[d]) return;
+    const int cnt = msg_received(rec, d, err);
+    int c = -1;
+    if (k < cnt) {
+        const float4 p = msg_data(rec, d)[2 * k];
+        c = ghost_cell(g, p.x, p.y, p.z);
+    }
+    const int r = warp_rank_in_cell(gcount, c);
+    if (k < cnt) grank[d * maxcap + k] = r;
+}
+
+__global__ void __launch_bounds__(256) k_ghost_scatter(Msgs rec, Geom g, int maxcap, const int *__restrict__ gstart,
+                                                       const int *__restrict__ grank, float4 *__restrict__ gpos,
+                                                       float4 *__restrict__ gvel)
+{
+    const int d = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (rec.cap[d] == 0) return;
+    const int cnt = min(*msg_count(rec, d), rec.cap[d]);
+    if (k >= cnt) return;
+    const float4 p = msg_data(rec, d)[2 * k];
+    const int dst = gstart[ghost_cell(g, p.x, p.y, p.z)] + grank[d * maxcap + k];
+    gpos[dst] = p;
+    gvel[dst] = msg_data(rec, d)[2 * k + 1];
+}
+
+// ---- row a9: one-sided local-ghost forces ------------------------------------------------
+// Local particle i in a boundary cell sums f_ij over the ghosts j of its halo neighbour
+// cells; the peer rank computes the exact negation for its own copy (global ids key the
+// RNG, C-19).  Runs after the interior pass on the same stream: plain read-modify-write.
+template <int KMODE>
+__global__ void __launch_bounds__(128) k_force_halo(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                                                    float4 *__restrict__ frc, const int *__restrict__ n_ptr,
+                                                    const float4 *__restrict__ gpos, const float4 *__restrict__ gvel,
+                                                    const int *__restrict__ gstart, Geom g, PairP pp,
+                                                    uint32_t s_lo, uint32_t s_hi)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= *n_ptr) return;
+    const float4 pi = pos[i];
+    const int ci[3] = {cell_coord(pi.x, g.inv_h[0], g.n[0]), cell_coord(pi.y, g.inv_h[1], g.n[1]),
+                       cell_coord(pi.z, g.inv_h[2], g.n[2])};
+    bool boundary = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) boundary |= g.split[k] && (ci[k] == 0 || ci[k] == g.n[k] - 1);
+    if (!boundary) return;
+    const float4 vi = vel[i];
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
+    const uint32_t idi = (uint32_t)__float_as_int(pi.w);
+    float Fx = 0.f, Fy = 0.f, Fz = 0.f;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int dd[3] = {dx, dy, dz};
+                int e[3];
+                float sh[3] = {0.f, 0.f, 0.f};
+                bool halo = false;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    int jc = ci[k] + dd[k];
+                    if (g.split[k]) {
+                        halo |= (jc < 0 || jc >= g.n[k]);
+                        e[k] = jc + 1;
+                    } else {
+                        if (jc < 0) { jc += g.n[k]; sh[k] = -g.L[k]; }
+                        else if (jc >= g.n[k]) { jc -= g.n[k]; sh[k] = g.L[k]; }
+                        e[k] = jc;
+                    }
+                }
+                if (!halo) continue;
+                const int c = e[0] + g.ext[0] * (e[1] + g.ext[1] * e[2]);
+                for (int j = gstart[c]; j < gstart[c + 1]; ++j) {
+                    const float4 pj = gpos[j];
+                    const float rx = pi.x - (pj.x + sh[0]), ry = pi.y - (pj.y + sh[1]), rz = pi.z - (pj.z + sh[2]);
+                    const float r2 = rx * rx + ry * ry + rz * rz;
+                    if (r2 < pp.rc2 && r2 > 0.0f) {
+                        const float4 vj = gvel[j];
+                        const float dv = rx * (vi.x - vj.x) + ry * (vi.y - vj.y) + rz * (vi.z - vj.z);
+                        const float s = pair_scalar<KMODE>(pp, r2, dv, idi, (uint32_t)__float_as_int(pj.w), ks);
+                        Fx += s * rx;
+                        Fy += s * ry;
+                        Fz += s * rz;
+                    }
+                }
+            }
+    float4 f = frc[i];
+    f.x += Fx;
+    f.y += Fy;
+    f.z += Fz;
+    frc[i] = f;
+}
+
+} // namespace dpd

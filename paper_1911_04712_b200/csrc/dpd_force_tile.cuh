@@ -65,6 +65,14 @@ struct ForceTileSmem {
     int overflow;                                // a capacity was exceeded -> fallback
 };
 
+// Extended-grid coordinate of interior cell coordinate c in [-1, n]: split dimensions
+// address their halo ring (index 0 / n + 1), periodic-local dimensions wrap.
+__device__ __forceinline__ int ext_coord(int c, int n, int split)
+{
+    if (split) return c + 1;
+    return c < 0 ? c + n : (c >= n ? c - n : c);
+}
+
 __device__ __forceinline__ int to_fixed(float f, float scale)
 {
     // round-to-nearest via the 1.5 * 2^23 magic constant; valid for |f * scale| < 2^22
@@ -309,19 +317,37 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
                               const int *__restrict__ start, const Geom &g, const PairP &pp, const FixP &fx,
                               uint32_t ks, PairRec &rec, int *err, int x0, int y0, int z0, int bx, int by, int bz)
 {
+    // home particle h of the tile -> (home cell, slot) by a scan over the <= 32 home cells
+    int nh = 0;
     for (int hc = 0; hc < bx * by * bz; ++hc) {
         const int cx = x0 + hc % bx, cy = y0 + (hc / bx) % by, cz = z0 + hc / (bx * by);
-        const int c0 = cx + g.ext[0] * (cy + g.ext[1] * cz);
-        for (int i = start[c0] + threadIdx.x; i < start[c0 + 1]; i += FT_NTHR) {
+        const int c0 = (cx + g.off[0]) + g.ext[0] * ((cy + g.off[1]) + g.ext[1] * (cz + g.off[2]));
+        nh += start[c0 + 1] - start[c0];
+    }
+    for (int h = threadIdx.x; h < nh; h += FT_NTHR) {
+        int hc = 0, base = 0, cx = 0, cy = 0, cz = 0, c0 = 0;
+        for (;; ++hc) {
+            cx = x0 + hc % bx;
+            cy = y0 + (hc / bx) % by;
+            cz = z0 + hc / (bx * by);
+            c0 = (cx + g.off[0]) + g.ext[0] * ((cy + g.off[1]) + g.ext[1] * (cz + g.off[2]));
+            const int cnt = start[c0 + 1] - start[c0];
+            if (h < base + cnt) break;
+            base += cnt;
+        }
+        const int i = start[c0] + (h - base);
+        {
             const float4 pi = pos[i], vi = vel[i];
             float Fx = 0.f, Fy = 0.f, Fz = 0.f;
             for (int o = 0; o < 14; ++o) {
-                int jx = cx + c_fwd[o][0], jy = cy + c_fwd[o][1], jz = cz + c_fwd[o][2];
+                const int jxi = cx + c_fwd[o][0], jyi = cy + c_fwd[o][1], jzi = cz + c_fwd[o][2];
                 float sx = 0.f, sy = 0.f, sz = 0.f;
-                if (jx < 0) { jx += g.n[0]; sx = -g.L[0]; } else if (jx >= g.n[0]) { jx -= g.n[0]; sx = g.L[0]; }
-                if (jy < 0) { jy += g.n[1]; sy = -g.L[1]; } else if (jy >= g.n[1]) { jy -= g.n[1]; sy = g.L[1]; }
-                if (jz >= g.n[2]) { jz -= g.n[2]; sz = g.L[2]; }
-                const int c = jx + g.ext[0] * (jy + g.ext[1] * jz);
+                if (!g.split[0]) sx = jxi < 0 ? -g.L[0] : (jxi >= g.n[0] ? g.L[0] : 0.f);
+                if (!g.split[1]) sy = jyi < 0 ? -g.L[1] : (jyi >= g.n[1] ? g.L[1] : 0.f);
+                if (!g.split[2]) sz = jzi >= g.n[2] ? g.L[2] : 0.f;
+                const int c = ext_coord(jxi, g.n[0], g.split[0]) +
+                              g.ext[0] * (ext_coord(jyi, g.n[1], g.split[1]) +
+                                          g.ext[1] * ext_coord(jzi, g.n[2], g.split[2]));
                 for (int j = (o == 0 ? i + 1 : start[c]); j < start[c + 1]; ++j) {
                     float4 pj = pos[j];
                     pj.x += sx;
@@ -374,12 +400,12 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0); // sza <= 3
         const int ly = row - lz * sya;
-        int gy = y0 - 1 + ly, gz = z0 + lz;
-        gy += (gy < 0) ? g.n[1] : (gy >= g.n[1] ? -g.n[1] : 0);
-        gz += (gz >= g.n[2]) ? -g.n[2] : 0;
+        // extended-grid coordinates: split dimensions index the halo ring (empty in the
+        // local lists) without wrapping; periodic-local dimensions wrap
+        const int gy = ext_coord(y0 - 1 + ly, g.n[1], g.split[1]);
+        const int gz = ext_coord(z0 + lz, g.n[2], g.split[2]);
         if (lane < sxa) {
-            int gx = x0 - 1 + lane;
-            gx += (gx < 0) ? g.n[0] : (gx >= g.n[0] ? -g.n[0] : 0);
+            const int gx = ext_coord(x0 - 1 + lane, g.n[0], g.split[0]);
             const int gc = gx + g.ext[0] * (gy + g.ext[1] * gz);
             const int a = start[gc];
             const int c = row * sxa + lane;
@@ -442,10 +468,10 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
         const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0);
         const int ly = row - lz * sya;
         const int gy = y0 - 1 + ly, gz = z0 + lz;
-        const float sy = gy < 0 ? -g.L[1] : (gy >= g.n[1] ? g.L[1] : 0.0f);
-        const float sz = gz >= g.n[2] ? g.L[2] : 0.0f;
+        const float sy = g.split[1] ? 0.0f : (gy < 0 ? -g.L[1] : (gy >= g.n[1] ? g.L[1] : 0.0f));
+        const float sz = g.split[2] ? 0.0f : (gz >= g.n[2] ? g.L[2] : 0.0f);
         const int c0 = sxa * row; // lx = 0
-        const bool wrap_lo = (x0 == 0), wrap_hi = (x0 + bx == g.n[0]);
+        const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
         const float sxl = wrap_lo ? -g.L[0] : 0.0f, sxh = wrap_hi ? g.L[0] : 0.0f;
         // segment A: lx = 0; B: lx = 1..bx; C: lx = bx + 1 (merged when not wrapped)
         const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
@@ -577,7 +603,7 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int c0 = sxa * row;
         const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
-        const bool wrap_lo = (x0 == 0), wrap_hi = (x0 + bx == g.n[0]);
+        const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
         const int gm = wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0];
         for (int s = a0 + lane; s < e0; s += 32) {

@@ -87,51 +87,147 @@ __device__ __forceinline__ int warp_rank_in_cell(int *count, int c)
 }
 
 // ---------------------------------------------------------------------------------------
-// Input packing (set_particles): AoS xyz -> pos4 (x, y, z, id bits), vel4; wrap (C-10).
+// Per-direction message buffers of the decomposition (ghosts and migrants).  Direction
+// D = (dx, dy, dz) in {-1,0,1}^3 has index d = (dx+1) + 3 (dy+1) + 9 (dz+1) (13 = none).
+// Message d starts at base + off[d] bytes: an int4 header {count, 0, 0, 0} followed by cap[d]
+// particles of two float4 each (x, y, z, id bits) and (u_x, u_y, u_z, 0).  cap[d] = 0 marks an
+// unused direction.  base == nullptr: single domain, no messages.
 // ---------------------------------------------------------------------------------------
-__global__ void k_pack_input(const float *__restrict__ pos3, const float *__restrict__ vel3,
-                             const int32_t *__restrict__ ids, int64_t n, Geom g, float4 *__restrict__ pos4,
-                             float4 *__restrict__ vel4, float4 *__restrict__ frc4, int *err)
+struct Msgs {
+    char *base;
+    int off[27];
+    int cap[27];
+};
+
+__device__ __forceinline__ int *msg_count(const Msgs &m, int d) { return reinterpret_cast<int *>(m.base + m.off[d]); }
+__device__ __forceinline__ float4 *msg_data(const Msgs &m, int d)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float x = pos3[3 * i + 0], y = pos3[3 * i + 1], z = pos3[3 * i + 2];
-    const float vx = vel3[3 * i + 0], vy = vel3[3 * i + 1], vz = vel3[3 * i + 2];
-    const int id = ids ? ids[i] : (int)i;
-    if (!finite3(x, y, z) || !finite3(vx, vy, vz)) {
-        raise_err(err, ERR_NONFINITE, id);
-        x = y = z = 0.0f;
-    }
-    // periodic wrap by whole multiples of L (input may lie several boxes away)
-    x = wrap_coord(x - g.L[0] * floorf(x / g.L[0]), g.L[0]);
-    y = wrap_coord(y - g.L[1] * floorf(y / g.L[1]), g.L[1]);
-    z = wrap_coord(z - g.L[2] * floorf(z / g.L[2]), g.L[2]);
-    pos4[i] = make_float4(x, y, z, __int_as_float(id));
-    vel4[i] = make_float4(vx, vy, vz, 0.0f);
-    frc4[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    return reinterpret_cast<float4 *>(m.base + m.off[d] + 16);
 }
 
 // ---------------------------------------------------------------------------------------
-// a1 + a2: kick, drift, wrap, cell index, atomic histogram.
+// Input packing (set_particles): AoS xyz -> pos4 (x, y, z, id bits), vel4; periodic wrap
+// into the global box (C-10), then (decomposed runs) keep only the particles inside this
+// rank's subdomain, in local coordinates.  *n_out counts the kept particles.
+// ---------------------------------------------------------------------------------------
+__global__ void k_pack_input(const float *__restrict__ pos3, const float *__restrict__ vel3,
+                             const int32_t *__restrict__ ids, int64_t n, Geom g, float3 gbox, float3 origin,
+                             float4 *__restrict__ pos4, float4 *__restrict__ vel4, float4 *__restrict__ frc4,
+                             int *n_out, int cap, int *err)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    float4 p4, v4;
+    if (i < n) {
+        float x = pos3[3 * i + 0], y = pos3[3 * i + 1], z = pos3[3 * i + 2];
+        const float vx = vel3[3 * i + 0], vy = vel3[3 * i + 1], vz = vel3[3 * i + 2];
+        const int id = ids ? ids[i] : (int)i;
+        if (!finite3(x, y, z) || !finite3(vx, vy, vz)) {
+            raise_err(err, ERR_NONFINITE, id);
+            x = y = z = 0.0f;
+        }
+        // periodic wrap by whole multiples of the global box (input may lie several boxes away)
+        x = wrap_coord(x - gbox.x * floorf(x / gbox.x), gbox.x);
+        y = wrap_coord(y - gbox.y * floorf(y / gbox.y), gbox.y);
+        z = wrap_coord(z - gbox.z * floorf(z / gbox.z), gbox.z);
+        x -= origin.x;
+        y -= origin.y;
+        z -= origin.z;
+        keep = x >= 0.0f && x < g.L[0] && y >= 0.0f && y < g.L[1] && z >= 0.0f && z < g.L[2];
+        p4 = make_float4(x, y, z, __int_as_float(id));
+        v4 = make_float4(vx, vy, vz, 0.0f);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(n_out, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+        const int slot = base + __popc(m & lanemask_lt());
+        if (slot < cap) {
+            pos4[slot] = p4;
+            vel4[slot] = v4;
+            frc4[slot] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        } else {
+            raise_err(err, ERR_CAPACITY, __float_as_int(p4.w));
+        }
+    }
+}
+
+// Number of input particles that fall inside this rank's subdomain (sizes the arrays).
+__global__ void k_count_inside(const float *__restrict__ pos3, int64_t n, float3 gbox, float3 origin, float3 sub,
+                               int *out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool in = false;
+    if (i < n) {
+        float x = pos3[3 * i + 0], y = pos3[3 * i + 1], z = pos3[3 * i + 2];
+        if (isfinite(x) && isfinite(y) && isfinite(z)) {
+            x = wrap_coord(x - gbox.x * floorf(x / gbox.x), gbox.x) - origin.x;
+            y = wrap_coord(y - gbox.y * floorf(y / gbox.y), gbox.y) - origin.y;
+            z = wrap_coord(z - gbox.z * floorf(z / gbox.z), gbox.z) - origin.z;
+            in = x >= 0.0f && x < sub.x && y >= 0.0f && y < sub.y && z >= 0.0f && z < sub.z;
+        } else {
+            in = origin.x == 0.0f && origin.y == 0.0f && origin.z == 0.0f; // reported by the pack kernel
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(out, __popc(m));
+}
+
+__device__ __forceinline__ int dir_index(int dx, int dy, int dz) { return (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1); }
+
+// ---------------------------------------------------------------------------------------
+// a1 + a2: kick, drift, wrap (periodic-local dimensions), cell index, atomic histogram.
+// In decomposed runs a particle that crossed a split face is a migrant (row a10): it is
+// shifted into the neighbour's frame and appended to the message of its exit direction;
+// rank = -1 drops it from the local sort.  The particle count comes from the device
+// (start_old[ncell]) so no host synchronisation is needed between steps.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_bin(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                                             const float4 *__restrict__ frc, int n, Geom g, IntegP ip,
-                                             int *__restrict__ count, int *__restrict__ rank, int *err)
+                                             const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
+                                             IntegP ip, int *__restrict__ count, int *__restrict__ rank, Msgs mig,
+                                             int *err)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = *n_ptr;
     int c = -1;
     if (i < n) {
         const float4 p = pos[i], v = vel[i], f = frc[i];
         float3 xn, un;
         advance(g, ip, p, v, f, xn, un);
-        if (!finite3(xn.x, xn.y, xn.z) || !finite3(un.x, un.y, un.z) || !in_local_box(g, xn)) {
-            raise_err(err, finite3(un.x, un.y, un.z) ? ERR_RANGE : ERR_NONFINITE, __float_as_int(p.w));
-            xn = make_float3(0.0f, 0.0f, 0.0f);
+        int dx = 0, dy = 0, dz = 0;
+        if (g.split[0]) dx = xn.x < 0.0f ? -1 : (xn.x >= g.L[0] ? 1 : 0);
+        if (g.split[1]) dy = xn.y < 0.0f ? -1 : (xn.y >= g.L[1] ? 1 : 0);
+        if (g.split[2]) dz = xn.z < 0.0f ? -1 : (xn.z >= g.L[2] ? 1 : 0);
+        if (dx | dy | dz) {
+            // migrant: into the destination frame
+            xn.x -= dx * g.L[0];
+            xn.y -= dy * g.L[1];
+            xn.z -= dz * g.L[2];
+            const int d = dir_index(dx, dy, dz);
+            if (!finite3(xn.x, xn.y, xn.z) || !in_local_box(g, xn)) {
+                raise_err(err, ERR_RANGE, __float_as_int(p.w));
+            } else {
+                const int slot = atomicAdd(msg_count(mig, d), 1);
+                if (slot < mig.cap[d]) {
+                    float4 *q = msg_data(mig, d) + 2 * slot;
+                    q[0] = make_float4(xn.x, xn.y, xn.z, p.w);
+                    q[1] = make_float4(un.x, un.y, un.z, 0.0f);
+                } else {
+                    raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
+                }
+            }
+        } else {
+            if (!finite3(xn.x, xn.y, xn.z) || !finite3(un.x, un.y, un.z) || !in_local_box(g, xn)) {
+                raise_err(err, finite3(un.x, un.y, un.z) ? ERR_RANGE : ERR_NONFINITE, __float_as_int(p.w));
+                xn = make_float3(0.0f, 0.0f, 0.0f);
+            }
+            c = cell_index(g, xn.x, xn.y, xn.z);
         }
-        c = cell_index(g, xn.x, xn.y, xn.z);
     }
     const int r = warp_rank_in_cell(count, c);
-    if (i < n) rank[i] = r;
+    if (i < n) rank[i] = (c >= 0) ? r : -1;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -267,13 +363,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, 
 // a4: scatter into cell order; recomputes a1 in registers (bit-identical to k_bin).
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                                                 const float4 *__restrict__ frc, int n, Geom g, IntegP ip,
-                                                 const int *__restrict__ start, const int *__restrict__ rank,
-                                                 float4 *__restrict__ pos_o, float4 *__restrict__ vel_o,
-                                                 float4 *__restrict__ frc_o)
+                                                 const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
+                                                 IntegP ip, const int *__restrict__ start,
+                                                 const int *__restrict__ rank, float4 *__restrict__ pos_o,
+                                                 float4 *__restrict__ vel_o, float4 *__restrict__ frc_o)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= *n_ptr || rank[i] < 0) return; // rank < 0: migrant, sent away
     const float4 p = pos[i], v = vel[i], f = frc[i];
     float3 xn, un;
     advance(g, ip, p, v, f, xn, un);
@@ -400,15 +496,15 @@ __global__ void k_ids_cells(const float4 *__restrict__ pos, int n, Geom g, int32
     if (cell_of_id) cell_of_id[id] = cell_index(g, p.x, p.y, p.z);
 }
 
-// Raw-state copy in storage order (x, u, F as float3 rows).
+// Raw-state copy in storage order (x in global coordinates, u, F as float3 rows).
 __global__ void k_state(const float4 *__restrict__ pos, const float4 *__restrict__ vel, const float4 *__restrict__ frc,
-                        int n, float *__restrict__ pos3, float *__restrict__ u3, float *__restrict__ f3,
-                        int32_t *__restrict__ ids)
+                        int n, float3 origin, float *__restrict__ pos3, float *__restrict__ u3,
+                        float *__restrict__ f3, int32_t *__restrict__ ids)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float4 p = pos[i], v = vel[i], f = frc[i];
-    if (pos3) { pos3[3 * i] = p.x; pos3[3 * i + 1] = p.y; pos3[3 * i + 2] = p.z; }
+    if (pos3) { pos3[3 * i] = p.x + origin.x; pos3[3 * i + 1] = p.y + origin.y; pos3[3 * i + 2] = p.z + origin.z; }
     if (u3) { u3[3 * i] = v.x; u3[3 * i + 1] = v.y; u3[3 * i + 2] = v.z; }
     if (f3) { f3[3 * i] = f.x; f3[3 * i + 1] = f.y; f3[3 * i + 2] = f.z; }
     if (ids) ids[i] = __float_as_int(p.w);

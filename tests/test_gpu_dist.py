@@ -1,0 +1,135 @@
+"""3D domain decomposition on one GPU: an
+in-process group of subdomain contexts exchanging ghosts and migrants by device copies runs
+the same kernels as the NCCL path.  Checked against the oracle's all-pairs sums (the plain
+definition, C-1) with the per-step protocol of C-13, plus particle/id conservation."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from test_gpu_parity import FORCE_TOL, boundary_eps, by_id, check_forces
+
+pytestmark = pytest.mark.gpu
+
+
+def make_group(cfg, grid):
+    from paper_1911_04712_b200 import capi
+    ctxs = capi.dpd_create_group(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed, grid)
+    return capi, ctxs
+
+
+def gather_state(capi, ctxs):
+    parts = [capi.dpd_get_state(c) for c in ctxs]
+    pos = np.concatenate([p[0] for p in parts])
+    u = np.concatenate([p[1] for p in parts])
+    f = np.concatenate([p[2] for p in parts])
+    ids = np.concatenate([p[3] for p in parts])
+    return pos, u, f, ids
+
+
+def destroy(capi, ctxs):
+    for c in ctxs:
+        capi.dpd_destroy(c)
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (3, 1, 2)])
+def test_group_prime_forces_match_oracle(grid):
+    cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
+    p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
+                         seed=cfg.seed)
+    pos0, vel0 = workloads.make_config(cfg)
+    capi, ctxs = make_group(cfg, grid)
+    try:
+        ids0 = np.arange(pos0.shape[0], dtype=np.int32)
+        for c in ctxs:  # every member receives the global set and keeps its own share
+            capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
+        capi.dpd_group_step(ctxs, 0)  # prime: ghost exchange + forces
+        counts = [capi.dpd_get_count(c) for c in ctxs]
+        assert sum(counts) == pos0.shape[0] and min(counts) > 0
+        pos, u, f, ids = gather_state(capi, ctxs)
+        assert np.array_equal(np.sort(ids), ids0)
+        x_id, u_id, f_id = by_id(ids, pos, u, f)
+        np.testing.assert_allclose(x_id, pos0, atol=1e-5)  # local frames map back exactly
+        F_ref, allow, _ = oracle.forces(p, x_id, u_id, 0, eps=boundary_eps(cfg.box))
+        check_forces(f_id, F_ref, allow)
+    finally:
+        destroy(capi, ctxs)
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 2)])
+def test_group_per_step_parity_with_migration(grid):
+    """30 steps at dt = 0.01 (config-1 parameters): particles migrate between subdomains; each
+    step the oracle recomputes F(x_s, u_s, s) from the gathered GPU state (C-13)."""
+    cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
+    p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
+                         seed=cfg.seed)
+    pos0, vel0 = workloads.make_config(cfg)
+    n = pos0.shape[0]
+    capi, ctxs = make_group(cfg, grid)
+    try:
+        ids0 = np.arange(n, dtype=np.int32)
+        for c in ctxs:
+            capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
+        capi.dpd_group_step(ctxs, 0)
+        start_counts = [capi.dpd_get_count(c) for c in ctxs]
+        for s in range(1, 31):
+            capi.dpd_group_step(ctxs, 1)
+            pos, u, f, ids = gather_state(capi, ctxs)
+            assert len(ids) == n and np.array_equal(np.sort(ids), ids0), "particles lost or duplicated"
+            assert all(capi.dpd_get_step(c) == s for c in ctxs)
+            x_id, u_id, f_id = by_id(ids, pos, u, f)
+            F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=boundary_eps(cfg.box))
+            check_forces(f_id, F_ref, allow)
+        moved = sum(abs(capi.dpd_get_count(c) - k) for c, k in zip(ctxs, start_counts))
+        assert moved > 0  # migration actually happened
+    finally:
+        destroy(capi, ctxs)
+
+
+def test_group_matches_single_domain():
+    """Same initial state on one domain and on a 2x2x2 group: forces after 5 steps agree to
+    fp32 accuracy (identical RNG words: global ids key the pair RNG, C-7/C-19)."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.with_box(workloads.CONFIGS["eq64"], (16.0, 16.0, 16.0))
+    pos0, vel0 = workloads.make_config(cfg)
+    single = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
+    single.set_particles(pos0, vel0)
+    _, ctxs = make_group(cfg, (2, 2, 2))
+    try:
+        ids0 = np.arange(pos0.shape[0], dtype=np.int32)
+        for c in ctxs:
+            capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
+        capi.dpd_group_step(ctxs, 0)
+        pos, u, f, ids = gather_state(capi, ctxs)
+        x1, u1, f1, ids1 = single.get_state()
+        a = by_id(ids, pos, f)
+        b = by_id(ids1, x1, f1)
+        np.testing.assert_allclose(a[0], b[0], atol=1e-5)
+        scale = np.abs(b[1]).max()
+        assert np.abs(a[1] - b[1]).max() < FORCE_TOL * scale
+    finally:
+        destroy(capi, ctxs)
+
+
+def test_group_temperature_and_momentum():
+    """Equilibrium on a 2x2x1 group (rho = 8, Table-2 parameters): T = kT within 1%
+    and total momentum conserved through migration and halo forces."""
+    cfg = workloads.with_box(workloads.CONFIGS["eq64"], (16.0, 16.0, 16.0))
+    pos0, vel0 = workloads.make_config(cfg)
+    capi, ctxs = make_group(cfg, (2, 2, 1))
+    try:
+        ids0 = np.arange(pos0.shape[0], dtype=np.int32)
+        for c in ctxs:
+            capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
+        capi.dpd_group_step(ctxs, 200)
+        Ts, Ps = [], []
+        for _ in range(60):
+            capi.dpd_group_step(ctxs, 10)
+            vs = np.concatenate([capi.dpd_get_particles_ex(c)[1] for c in ctxs]).astype(np.float64)
+            assert vs.shape[0] == pos0.shape[0]
+            Ts.append(oracle.temperature(vs))
+            Ps.append(vs.sum(axis=0))
+        assert abs(np.mean(Ts) - 1.0) < 0.01, np.mean(Ts)
+        assert np.abs(np.array(Ps)).max() < 1e-2 * np.sqrt(pos0.shape[0])
+    finally:
+        destroy(capi, ctxs)
