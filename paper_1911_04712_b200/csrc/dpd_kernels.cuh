@@ -201,10 +201,14 @@ __global__ void __launch_bounds__(256) k_bin(const float4 *__restrict__ pos, con
         if (g.split[1]) dy = xn.y < 0.0f ? -1 : (xn.y >= g.L[1] ? 1 : 0);
         if (g.split[2]) dz = xn.z < 0.0f ? -1 : (xn.z >= g.L[2] ? 1 : 0);
         if (dx | dy | dz) {
-            // migrant: into the destination frame
+            // migrant: into the destination frame.  x - (-L) = x + L can round up to L for
+            // x within an ulp below 0; keep it inside [0, L) (the C-10 rule for wrapped axes)
             xn.x -= dx * g.L[0];
             xn.y -= dy * g.L[1];
             xn.z -= dz * g.L[2];
+            if (dx < 0 && xn.x >= g.L[0]) xn.x = __int_as_float(__float_as_int(g.L[0]) - 1);
+            if (dy < 0 && xn.y >= g.L[1]) xn.y = __int_as_float(__float_as_int(g.L[1]) - 1);
+            if (dz < 0 && xn.z >= g.L[2]) xn.z = __int_as_float(__float_as_int(g.L[2]) - 1);
             const int d = dir_index(dx, dy, dz);
             if (!finite3(xn.x, xn.y, xn.z) || !in_local_box(g, xn)) {
                 raise_err(err, ERR_RANGE, __float_as_int(p.w));
