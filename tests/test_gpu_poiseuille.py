@@ -1,0 +1,72 @@
+"""Periodic Poiseuille flow on the CUDA path (§4.2; reading C-16) and
+the viscosity measurement of NEXT-1 against a Table-1 row.
+
+Body force f_z = -f for x <= L/2, +f otherwise; steady profile
+v_z(x) = -rho f (x L/2 - x^2) / (2 eta) on [0, L/2], mirrored on (L/2, L].
+eta is fitted per half (least squares on the closed form)."""
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def run_profile(cfg, f, warm, nsample, every, nbins):
+    from paper_1911_04712_b200 import capi
+    pos0, vel0 = workloads.make_config(cfg)
+    d = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
+    d.set_body_force(f)
+    d.set_particles(pos0, vel0)
+    d.step(warm)
+    L = cfg.box[0]
+    acc = np.zeros(nbins)
+    cnt = np.zeros(nbins)
+    for _ in range(nsample):
+        d.step(every)
+        x, v = d.get_particles()
+        b = np.minimum((x[:, 0] / L * nbins).astype(int), nbins - 1)
+        acc += np.bincount(b, weights=v[:, 2], minlength=nbins)
+        cnt += np.bincount(b, minlength=nbins)
+    xc = (np.arange(nbins) + 0.5) * L / nbins
+    return xc, acc / cnt
+
+
+def fit_eta(xc, vz, L, rho, f):
+    """Least-squares eta per half: v = -rho f (x L/2 - x^2) / (2 eta) on [0, L/2] and the mirror
+    image v = +rho f (x' L/2 - x'^2) / (2 eta), x' = x - L/2, on (L/2, L]."""
+    lo = xc <= L / 2
+    g_lo = -rho * f * (xc[lo] * L / 2 - xc[lo] ** 2) / 2
+    xh = xc[~lo] - L / 2
+    g_hi = rho * f * (xh * L / 2 - xh ** 2) / 2
+    inv_lo = np.dot(g_lo, vz[lo]) / np.dot(g_lo, g_lo)
+    inv_hi = np.dot(g_hi, vz[~lo]) / np.dot(g_hi, g_hi)
+    model = np.concatenate([g_lo / (1 / inv_lo), g_hi / (1 / inv_hi)])
+    l2 = np.linalg.norm(model - vz) / np.linalg.norm(vz)
+    return 1 / inv_lo, 1 / inv_hi, l2
+
+
+def test_periodic_poiseuille_parabola_fig3_parameters():
+    # Fig.-3 parameters: rho = 8, a = 10, gamma = 20, kT = 1, k = 0.5, dt = 0.005
+    cfg = workloads.with_box(workloads.CONFIGS["pois96"], (16.0, 16.0, 16.0))
+    f = 0.05
+    xc, vz = run_profile(cfg, f, warm=4000, nsample=300, every=10, nbins=16)
+    eta_lo, eta_hi, l2 = fit_eta(xc, vz, 16.0, 8.0, f)
+    # L2 error of the parabola < 5 %, the two half-domain fits agree within 5 %
+    assert l2 < 0.05, (l2, vz)
+    assert abs(eta_lo - eta_hi) / (0.5 * (eta_lo + eta_hi)) < 0.05, (eta_lo, eta_hi)
+    # flow direction follows the force: -z on the lower half, +z on the upper half (C-16)
+    assert vz[: len(vz) // 2].mean() < 0 < vz[len(vz) // 2:].mean()
+
+
+@pytest.mark.slow
+def test_viscosity_groot_warren_table1_row():
+    # Table 1 row: a = 25, gamma = 6.75, rho = 3, k = 1, kT = 1, rc = 1, dt = 0.04;
+    # Mirheo eta = 0.89-0.9, reference 0.91 [Groot1997]; acceptance [0.85, 0.97]
+    cfg = workloads.Config("gw", (16.0, 16.0, 16.0), 3.0, 25.0, 6.75, 1.0, 1.0, 0.04)
+    f = 0.01
+    xc, vz = run_profile(cfg, f, warm=3000, nsample=400, every=10, nbins=16)
+    eta_lo, eta_hi, l2 = fit_eta(xc, vz, 16.0, 3.0, f)
+    eta = 0.5 * (eta_lo + eta_hi)
+    assert l2 < 0.1, l2
+    assert 0.85 <= eta <= 0.97, (eta_lo, eta_hi)
