@@ -221,6 +221,7 @@ def main():
     ap.add_argument("--impl", default="dpd", choices=["dpd", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-kernel", type=int, default=None, help="0 tiled, 1 reference, 2 cell-warp")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = workloads.CONFIGS[args.config]
@@ -258,6 +259,8 @@ def main():
     else:
         ctx = capi.dpd_create(gbox, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
     capi.dpd_set_stream(ctx, stream.cuda_stream)
+    if args.force_kernel is not None:
+        capi.dpd_set_option(ctx, "force_kernel", args.force_kernel)
     if cfg.body_f:
         capi.dpd_set_body_force(ctx, cfg.body_f)
     # each rank generates only its own subdomain's particles with globally unique ids

@@ -32,6 +32,7 @@
 
 #include "../../include/dpd.h"
 #include "dpd_dist.cuh"
+#include "dpd_force_cells.cuh"
 #include "dpd_force_tile.cuh"
 #include "dpd_kernels.cuh"
 
@@ -380,6 +381,32 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const Geom g = c->geom;
     const PairP pp = c->pp;
+    if (c->force_impl == 2) {
+        const FixP fx = c->fix;
+        const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
+                          ((g.n[2] + FT_BZ - 1) / FT_BZ);
+        const size_t smem = sizeof(ForceCellSmem);
+        const int *st = c->start[c->scur].p;
+        return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
+#define DPD_CELLS(R, K)                                                                                             \
+    k_force_cells<R, K><<<ntile, FC_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, s_lo, \
+                                                             s_hi, rec, c->err.p)
+            if (record) {
+                switch (c->kmode) {
+                case 0: DPD_CELLS(true, 0); break;
+                case 1: DPD_CELLS(true, 1); break;
+                default: DPD_CELLS(true, 2); break;
+                }
+            } else {
+                switch (c->kmode) {
+                case 0: DPD_CELLS(false, 0); break;
+                case 1: DPD_CELLS(false, 1); break;
+                default: DPD_CELLS(false, 2); break;
+                }
+            }
+#undef DPD_CELLS
+        });
+    }
     if (c->force_impl == 0 || c->dist) {
         const FixP fx = c->fix;
         const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
@@ -732,6 +759,15 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxShared));
         }
+        const int smc = (int)sizeof(ForceCellSmem);
+        const void *fcs[6] = {(const void *)k_force_cells<false, 0>, (const void *)k_force_cells<false, 1>,
+                              (const void *)k_force_cells<false, 2>, (const void *)k_force_cells<true, 0>,
+                              (const void *)k_force_cells<true, 1>,  (const void *)k_force_cells<true, 2>};
+        for (const void *f : fcs) {
+            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smc));
+            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared));
+        }
     }
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
@@ -913,7 +949,8 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
 {
     if (!c || !name) return DPD_ERR_ARG;
     if (strcmp(name, "force_kernel") == 0) {
-        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled) or 1 (reference)");
+        if (value < 0 || value > 2)
+            return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled), 1 (reference) or 2 (cell-warp)");
         if (value == 1 && c->dist) return fail(c, DPD_ERR_ARG, "the reference kernel is single-domain only");
         c->force_impl = (int)value;
         return DPD_OK;

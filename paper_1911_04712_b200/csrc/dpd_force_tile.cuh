@@ -324,7 +324,7 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
         const int c0 = (cx + g.off[0]) + g.ext[0] * ((cy + g.off[1]) + g.ext[1] * (cz + g.off[2]));
         nh += start[c0 + 1] - start[c0];
     }
-    for (int h = threadIdx.x; h < nh; h += FT_NTHR) {
+    for (int h = threadIdx.x; h < nh; h += blockDim.x) {
         int hc = 0, base = 0, cx = 0, cy = 0, cz = 0, c0 = 0;
         for (;; ++hc) {
             cx = x0 + hc % bx;

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 FORCE_TOL = 1e-4
 
 
-KERNELS = [0, 1]  # 0: tiled production kernel, 1: reference kernel
+KERNELS = [0, 1, 2]  # 0: tiled, 1: reference, 2: cell-warp
 
 
 def _ctx(cfg, seed=None, kernel=0):
