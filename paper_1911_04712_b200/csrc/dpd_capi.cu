@@ -747,6 +747,10 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
         c->fix.scale = (float)std::ldexp(1.0, k);
         c->fix.inv_scale = (float)std::ldexp(1.0, -k);
         c->fix.mag_lim = (float)std::ldexp(1.0, 21 - k);
+        // row-end pruning slack: far above the cell-binning rounding of
+        // coordinates up to the box extent, far below any cell size
+        const double lmax = std::max(box[0], std::max(box[1], box[2]));
+        c->fix.slack = (float)(1e-4 + lmax * std::ldexp(1.0, -20));
     }
     {
         // two tiles per SM need the maximum shared-memory carveout (2 x (smem + 1 KB) <= 228 KB)

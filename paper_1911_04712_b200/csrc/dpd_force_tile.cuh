@@ -35,30 +35,29 @@ constexpr int FT_SCAP = 1152;                 // staged particles (mean 864, sd 
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
 constexpr int FT_LCAP = 48;                   // hits per home particle (mean 16.8)
 constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 25 words per list (odd): conflict-free appends
+constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32 owners + sentinel)
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
 struct FixP {
     float scale;     // 2^k
     float inv_scale; // 2^-k
     float mag_lim;   // 2^21 / scale: larger pair magnitudes raise ERR_RANGE
+    float slack;     // row-end pruning: distance bounds are lowered by this much
 };
 
 struct ForceTileSmem {
     float4 sp[FT_SCAP];                          // staged positions (tile frame), w = id bits
     float4 sv[FT_SCAP];                          // staged velocities
-    float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // SoA copy of the positions for the sweep
+    float sx[FT_SCAP + 4], sy[FT_SCAP + 4], sz[FT_SCAP + 4]; // SoA positions (sweep; +4: masked over-reads)
     int acc[3][FT_SCAP];                         // fixed-point force sums
-    unsigned short lst[FT_HCAP * FT_LSTRIDE];    // per-home-particle pair lists
-    int oexcl[FT_HCAP + 1];                      // compacted owners: list prefix (+ total)
-    int osi[FT_HCAP];                            //   staged index of the owner
-    int orow[FT_HCAP];                           //   list base minus prefix
-    int hcnt[FT_HCAP];                           // hits per home particle
-    int hsi[FT_HCAP];                            // staged index per home particle
+    unsigned short lst[FT_NTHR * FT_LSTRIDE];    // per-thread pair lists (one home particle each)
+    int woex[FT_NWARP * FT_WSTRIDE];             // per warp: compacted owners' list prefix (+ total)
+    int wsi[FT_NWARP * FT_WSTRIDE];              //   staged index of the owner
+    int wrow[FT_NWARP * FT_WSTRIDE];             //   list base minus prefix
     int soff[FT_NSC + 1];                        // staged cell -> smem start (exclusive scan)
     int cgs[FT_NSC];                             // staged cell -> global start
     int scnt[FT_NSC];                            // staged cell -> particle count
     int hoff[FT_NHROW + 1];                      // home row -> first home index (prefix)
-    int wsum[FT_NWARP];                          // block-scan scratch
     int tile[4];                                 // x0, y0, z0 of this tile
     int total;                                   // staged particles
     int nown;                                    // owners with a non-empty list
@@ -89,6 +88,16 @@ __device__ __forceinline__ void append_if(unsigned &lptr, float r2, float rc2, u
                  "@p add.u32 %0, %0, 2;\n\t}"
                  : "+r"(lptr)
                  : "f"(r2), "f"(rc2), "r"(j)
+                 : "memory");
+}
+
+// Append j if r2 < rc2 and j < hi (candidate masking at a segment's end).
+__device__ __forceinline__ void append_if_below(unsigned &lptr, float r2, float rc2, unsigned j, unsigned hi)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tsetp.lt.and.u32 p, %3, %4, p;\n\t"
+                 "@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
+                 : "+r"(lptr)
+                 : "f"(r2), "f"(rc2), "r"(j), "r"(hi)
                  : "memory");
 }
 
@@ -135,55 +144,70 @@ __device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, in
         ++j;
     }
     const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
-    for (; j + 1 < hi; j += 2) {
+    // four candidates per iteration: two independent packed chains in flight (ILP)
+    for (; j + 3 < hi; j += 4) {
+        float ra, rb, rc, rd;
+        r2_pair(ld_f2(&S.sx[j]), ld_f2(&S.sy[j]), ld_f2(&S.sz[j]), PX, PY, PZ, ra, rb);
+        r2_pair(ld_f2(&S.sx[j + 2]), ld_f2(&S.sy[j + 2]), ld_f2(&S.sz[j + 2]), PX, PY, PZ, rc, rd);
+        append_if(lptr, ra, rc2, (unsigned)j);
+        append_if(lptr, rb, rc2, (unsigned)(j + 1));
+        append_if(lptr, rc, rc2, (unsigned)(j + 2));
+        append_if(lptr, rd, rc2, (unsigned)(j + 3));
+    }
+    if (j + 1 < hi) {
         float ra, rb;
         r2_pair(ld_f2(&S.sx[j]), ld_f2(&S.sy[j]), ld_f2(&S.sz[j]), PX, PY, PZ, ra, rb);
         append_if(lptr, ra, rc2, (unsigned)j);
         append_if(lptr, rb, rc2, (unsigned)(j + 1));
+        j += 2;
     }
     if (j < hi) append_if(lptr, r2_one(S, j, px, py, pz), rc2, (unsigned)j);
 }
 
-// Contiguous copy of global particles [g0, g0 + len) to smem [s0, s0 + len) with a shift.
-__device__ __forceinline__ void stage_segment(ForceTileSmem &S, const float4 *__restrict__ pos,
-                                              const float4 *__restrict__ vel, int g0, int s0, int len, float sx,
-                                              float sy, float sz, int lane)
+// Asynchronous copy (LDGSTS, no register round trip) of global particles [g0, g0 + len)
+// to smem [s0, s0 + len): every load of the tile is in flight before any is waited for.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+
+__device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__restrict__ pos,
+                                           const float4 *__restrict__ vel, int g0, int s0, int len, int lane)
 {
     for (int k = lane; k < len; k += 32) {
-        const float4 p = pos[g0 + k];
+        cp_async16(&S.sp[s0 + k], &pos[g0 + k]);
+        cp_async16(&S.sv[s0 + k], &vel[g0 + k]);
+    }
+}
+
+// Second pass over a staged range: periodic-image shift, SoA copy, zeroed accumulators.
+__device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, float sx, float sy, float sz, int lane)
+{
+    for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
+        const float4 p = S.sp[s];
         const float px = p.x + sx, py = p.y + sy, pz = p.z + sz;
         S.sp[s] = make_float4(px, py, pz, p.w);
         S.sx[s] = px;
         S.sy[s] = py;
         S.sz[s] = pz;
-        S.sv[s] = vel[g0 + k];
         S.acc[0][s] = 0;
         S.acc[1][s] = 0;
         S.acc[2][s] = 0;
     }
 }
 
-// Block-wide exclusive scan of one int per thread (FT_NTHR threads); returns the total.
-__device__ __forceinline__ int block_excl_scan(ForceTileSmem &S, int v, int &excl, int lane, int warp)
+// Warp-wide inclusive scan of one int per lane.
+__device__ __forceinline__ int warp_incl_scan(int v, int lane)
 {
-    int incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
     }
-    if (lane == 31) S.wsum[warp] = incl;
-    __syncthreads();
-    int before = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < FT_NWARP; ++w) {
-        const int s = S.wsum[w];
-        before += (w < warp) ? s : 0;
-        total += s;
-    }
-    excl = before + incl - v;
-    return total;
+    return v;
 }
 
 // Pair evaluation shared by the fast path (smem operands) and the record path.
@@ -247,28 +271,29 @@ __device__ __forceinline__ void pair_checks(const PairP &pp, const FixP &fx, flo
     }
 }
 
-// Walk over a contiguous range [t, t1) of the CTA-wide pair list.  Owners (home particles
-// with a non-empty list) change at most a few times per range; the i-side fixed-point sum
-// is kept in registers and flushed on each owner change.
+// Walk over a contiguous range [t, t1) of one warp's concatenated pair lists.  Owners (home
+// particles with a non-empty list) change at most a few times per range; the i-side
+// fixed-point sum is kept in registers and flushed on each owner change.  `o` indexes the
+// warp's owner table (woex/wsi/wrow at stride FT_WSTRIDE).
 struct PairCursor {
     int t, t1, o, enext, si, lrow;
     float4 pi, vi;
     int fx, fy, fz;
 };
 
-__device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &S, int t0, int t1, int nown)
+__device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &S, int t0, int t1, int base, int nown)
 {
     c.t = t0;
     c.t1 = t1;
     c.fx = c.fy = c.fz = 0;
-    int o = 0; // largest owner slot with oexcl[o] <= t0
+    int o = 0; // largest owner slot with woex[o] <= t0
 #pragma unroll
-    for (int step = 256; step > 0; step >>= 1)
-        if (o + step < nown && S.oexcl[o + step] <= t0) o += step;
-    c.o = o;
-    c.enext = S.oexcl[o + 1];
-    c.si = S.osi[o];
-    c.lrow = S.orow[o];
+    for (int step = 16; step > 0; step >>= 1)
+        if (o + step < nown && S.woex[base + o + step] <= t0) o += step;
+    c.o = base + o;
+    c.enext = S.woex[c.o + 1];
+    c.si = S.wsi[c.o];
+    c.lrow = S.wrow[c.o];
     c.pi = S.sp[c.si];
     c.vi = S.sv[c.si];
 }
@@ -289,9 +314,9 @@ __device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
     if (c.t >= c.enext) { // next owner (never empty)
         cursor_flush(c, S);
         ++c.o;
-        c.enext = S.oexcl[c.o + 1];
-        c.si = S.osi[c.o];
-        c.lrow = S.orow[c.o];
+        c.enext = S.woex[c.o + 1];
+        c.si = S.wsi[c.o];
+        c.lrow = S.wrow[c.o];
         c.pi = S.sp[c.si];
         c.vi = S.sv[c.si];
     }
@@ -463,138 +488,159 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
         return;
     }
 
-    // ---- 1b. stage rows: each row is <= 3 contiguous global segments -----------------
+    // ---- 1b. stage rows: each row is <= 3 contiguous global segments; all copies of the
+    //          warp are issued first (async), then each row is shifted / transposed
+    const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
+    for (int row = warp; row < sya * sza; row += FT_NWARP) {
+        const int c0 = sxa * row; // lx = 0
+        // segment A: lx = 0; B: lx = 1..bx; C: lx = bx + 1 (merged when not wrapped)
+        const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
+        const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
+        if (wrap_lo) stage_copy(S, pos, vel, S.cgs[c0], a0, b0 - a0, lane);
+        stage_copy(S, pos, vel, wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0], mlo, mhi - mlo, lane);
+        if (wrap_hi) stage_copy(S, pos, vel, S.cgs[c0 + bx + 1], c0s, e0 - c0s, lane);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0);
         const int ly = row - lz * sya;
         const int gy = y0 - 1 + ly, gz = z0 + lz;
         const float sy = g.split[1] ? 0.0f : (gy < 0 ? -g.L[1] : (gy >= g.n[1] ? g.L[1] : 0.0f));
         const float sz = g.split[2] ? 0.0f : (gz >= g.n[2] ? g.L[2] : 0.0f);
-        const int c0 = sxa * row; // lx = 0
-        const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
-        const float sxl = wrap_lo ? -g.L[0] : 0.0f, sxh = wrap_hi ? g.L[0] : 0.0f;
-        // segment A: lx = 0; B: lx = 1..bx; C: lx = bx + 1 (merged when not wrapped)
+        const int c0 = sxa * row;
         const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
-        if (wrap_lo) stage_segment(S, pos, vel, S.cgs[c0], a0, b0 - a0, sxl, sy, sz, lane);
-        const int mlo = wrap_lo ? b0 : a0;
-        const int mhi = wrap_hi ? c0s : e0;
-        const int gm = wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0];
-        stage_segment(S, pos, vel, gm, mlo, mhi - mlo, 0.0f, sy, sz, lane);
-        if (wrap_hi) stage_segment(S, pos, vel, S.cgs[c0 + bx + 1], c0s, e0 - c0s, sxh, sy, sz, lane);
+        const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
+        if (wrap_lo) stage_fix(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
+        stage_fix(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
+        if (wrap_hi) stage_fix(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
     }
     __syncthreads();
 
-    // ---- 2. sweep: one home particle per thread (a second round only past FT_NTHR) -------
+    // ---- 2-4. per warp, one home particle per lane (a second round only past FT_NTHR):
+    //           sweep the lane's 5 segments into its list, then evaluate the warp's pairs
+    //           with a warp-balanced split -- no CTA barrier between sweep and pairs
     const int rowz = sxa * sya;
-    for (int h = tid; h < nhome; h += FT_NTHR) {
-        int r = 0;
-        while (r + 1 < by * bz && S.hoff[r + 1] <= h) ++r;
-        const int lz = r >= by ? 1 : 0;
-        const int ly = 1 + r - lz * by;
-        const int crow = sxa * (ly + sya * lz);
-        const int s_i = S.soff[crow + 1] + (h - S.hoff[r]);
-        int lx = 1;
-        while (lx < bx && S.soff[crow + lx + 1] <= s_i) ++lx;
-        const int c = crow + lx;
-        const int c1 = c - 1 + sxa; // (lx - 1, ly + 1, lz): the y+1 row
-        const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
-        const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[h * FT_LSTRIDE]);
-        unsigned lptr = lbase;
-        bool full = false;
+    const float hx = g.L[0] / (float)g.n[0], hy = g.L[1] / (float)g.n[1], hz = g.L[2] / (float)g.n[2];
+    const int wb = warp * FT_WSTRIDE;
+    const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[tid * FT_LSTRIDE]);
+    // warp w owns home particles [w nhome / NWARP, (w + 1) nhome / NWARP): equal counts, so
+    // no warp idles at the flush barrier for want of particles
+    const int hend = ((warp + 1) * nhome) / FT_NWARP;
+    for (int hb = (warp * nhome) / FT_NWARP; hb < hend; hb += 32) {
+        const int h = hb + lane;
+        int cnt = 0, s_i = 0;
+        if (h < hend) {
+            int r = 0;
+            while (r + 1 < by * bz && S.hoff[r + 1] <= h) ++r;
+            const int lz = r >= by ? 1 : 0;
+            const int ly = 1 + r - lz * by;
+            const int crow = sxa * (ly + sya * lz);
+            s_i = S.soff[crow + 1] + (h - S.hoff[r]);
+            int lx = 1;
+            while (lx < bx && S.soff[crow + lx + 1] <= s_i) ++lx;
+            const int c = crow + lx;
+            const int c1 = c - 1 + sxa; // (lx - 1, ly + 1, lz): the y+1 row
+            const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
+            // row-end pruning: lower bounds (minus a rounding slack) on the distance from i
+            // to its cell's faces; a row / end cell farther than r_c holds no partner
+            const float ox = px - (float)(x0 + lx - 1) * hx, oy = py - (float)(y0 + ly - 1) * hy,
+                        oz = pz - (float)(z0 + lz) * hz;
+            const float dxl = fmaxf(ox - fx.slack, 0.0f), dxr = fmaxf(hx - ox - fx.slack, 0.0f);
+            const float dyl = fmaxf(oy - fx.slack, 0.0f), dyr = fmaxf(hy - oy - fx.slack, 0.0f);
+            const float dzr = fmaxf(hz - oz - fx.slack, 0.0f);
+            unsigned lptr = lbase;
+            bool full = false;
 #pragma unroll 1
-        for (int k = 0; k < 5; ++k) {
-            // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
-            const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
-            int a = (k == 0) ? s_i + 1 : S.soff[cs];
-            const int b = S.soff[cs + (k == 0 ? 2 : 3)];
-            // a chunk of m candidates adds at most m entries: sweep in chunks that fit the
-            // remaining list capacity; once the list is full (first particle of a crowded
-            // cell, ~4 sigma) the remaining candidates are evaluated in place
-            while (a < b) {
-                const int room = FT_LCAP - (int)((lptr - lbase) >> 1);
-                if (room <= 0) {
-                    full = true;
-                    break;
+            for (int k = 0; k < 5; ++k) {
+                // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
+                const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
+                int a = (k == 0) ? s_i + 1 : S.soff[cs];
+                int b = S.soff[cs + (k == 0 ? 2 : 3)];
+                if (k > 0) {
+                    const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
+                    const float qz = (k == 1) ? 0.0f : dzr;
+                    const float q = qy * qy + qz * qz;
+                    if (!(q < pp.rc2)) continue;
+                    if (!(dxl * dxl + q < pp.rc2)) a = S.soff[cs + 1];
+                    if (!(dxr * dxr + q < pp.rc2)) b = S.soff[cs + 2];
                 }
-                const int e = min(b, a + room);
-                sweep(S, lptr, a, e, px, py, pz, pp.rc2);
-                a = e;
-            }
-            if (full) {
-                const float4 pi = S.sp[s_i], vi = S.sv[s_i];
-                for (; a < b; ++a) {
-                    if (!(r2_one(S, a, px, py, pz) < pp.rc2)) continue;
-                    float dx, dy, dz;
-                    const float s = pair_eval<RECORD, KMODE>(pp, fx, pi, vi, S.sp[a], S.sv[a], ks, rec, err, dx, dy, dz);
-                    const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
-                              qz = to_fixed(s * dz, fx.scale);
-                    atomicAdd(&S.acc[0][s_i], qx);
-                    atomicAdd(&S.acc[1][s_i], qy);
-                    atomicAdd(&S.acc[2][s_i], qz);
-                    atomicAdd(&S.acc[0][a], -qx);
-                    atomicAdd(&S.acc[1][a], -qy);
-                    atomicAdd(&S.acc[2][a], -qz);
+                // a chunk of m candidates adds at most m entries: sweep in chunks that fit the
+                // remaining list capacity; once the list is full (first particle of a crowded
+                // cell, ~4 sigma) the remaining candidates are evaluated in place
+                while (a < b) {
+                    const int room = FT_LCAP - (int)((lptr - lbase) >> 1);
+                    if (room <= 0) {
+                        full = true;
+                        break;
+                    }
+                    const int e = min(b, a + room);
+                    sweep(S, lptr, a, e, px, py, pz, pp.rc2);
+                    a = e;
+                }
+                if (full) {
+                    const float4 pi = S.sp[s_i], vi = S.sv[s_i];
+                    for (; a < b; ++a) {
+                        if (!(r2_one(S, a, px, py, pz) < pp.rc2)) continue;
+                        float dx, dy, dz;
+                        const float s =
+                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, S.sp[a], S.sv[a], ks, rec, err, dx, dy, dz);
+                        const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
+                                  qz = to_fixed(s * dz, fx.scale);
+                        atomicAdd(&S.acc[0][s_i], qx);
+                        atomicAdd(&S.acc[1][s_i], qy);
+                        atomicAdd(&S.acc[2][s_i], qz);
+                        atomicAdd(&S.acc[0][a], -qx);
+                        atomicAdd(&S.acc[1][a], -qy);
+                        atomicAdd(&S.acc[2][a], -qz);
+                    }
                 }
             }
+            if (full) atomicAdd(&err[6], 1); // statistics: in-place evaluations
+            cnt = (int)(lptr - lbase) >> 1;
         }
-        if (full && tid == h) atomicAdd(&err[6], 1); // statistics: in-place evaluations
-        S.hcnt[h] = (int)(lptr - lbase) >> 1;
-        S.hsi[h] = s_i;
-    }
-    __syncthreads();
 
-    // ---- 3. compacted owner table and CTA-wide prefix over the list lengths -------------
-    // thread t handles home particles t and t + FT_NTHR (nhome <= FT_HCAP < 2 FT_NTHR)
-    const int h0 = tid, h1 = tid + FT_NTHR;
-    const int n0 = h0 < nhome ? S.hcnt[h0] : 0, n1 = h1 < nhome ? S.hcnt[h1] : 0;
-    const int k0 = n0 > 0, k1 = n1 > 0;
-    int pexcl = 0, oexcl = 0;
-    // two scans packed into one: low 16 bits = owners, high 16 bits = entries
-    const int packed_tot = block_excl_scan(S, (k0 + k1) | ((n0 + n1) << 16), pexcl, lane, warp);
-    oexcl = pexcl & 0xFFFF;
-    int eexcl = pexcl >> 16;
-    if (k0) {
-        S.oexcl[oexcl] = eexcl;
-        S.osi[oexcl] = S.hsi[h0];
-        S.orow[oexcl] = h0 * FT_LSTRIDE - eexcl;
-        ++oexcl;
-        eexcl += n0;
-    }
-    if (k1) {
-        S.oexcl[oexcl] = eexcl;
-        S.osi[oexcl] = S.hsi[h1];
-        S.orow[oexcl] = h1 * FT_LSTRIDE - eexcl;
-    }
-    const int nown = packed_tot & 0xFFFF;
-    const int tot = packed_tot >> 16;
-    if (tid == 0) S.oexcl[nown] = tot;
-    __syncthreads();
-
-    // ---- 4. pair evaluation: contiguous chunk of the CTA-wide list per thread, walked by
-    //         two independent cursors (halves of the chunk) so two Philox/Box-Muller chains
-    //         are in flight per thread (instruction-level parallelism at 2 CTAs / SM)
-    {
-        const int C = (tot + FT_NTHR - 1) / FT_NTHR;
-        const int t0 = min(tid * C, tot);
-        const int t1 = min(t0 + C, tot);
-        const int tm = t0 + ((t1 - t0 + 1) >> 1);
-        PairCursor A, B;
-        cursor_init(A, S, t0, tm, nown);
-        cursor_init(B, S, tm, t1, nown);
-        while (A.t < A.t1) { // B is never longer than A
-            const int ja = cursor_next(A, S);
-            const bool bact = B.t < B.t1;
-            const int jb = bact ? cursor_next(B, S) : B.si; // inactive: self pair, r2 = 0 -> f = 0
-            float dxa, dya, dza, dxb, dyb, dzb;
-            const float sa = pair_core<KMODE>(pp, A.pi, A.vi, S.sp[ja], S.sv[ja], ks, dxa, dya, dza);
-            const float sb = pair_core<KMODE>(pp, B.pi, B.vi, S.sp[jb], S.sv[jb], ks, dxb, dyb, dzb);
-            pair_checks<RECORD>(pp, fx, A.pi, S.sp[ja], sa, dxa, dya, dza, ks, rec, err);
-            if (bact) pair_checks<RECORD>(pp, fx, B.pi, S.sp[jb], sb, dxb, dyb, dzb, ks, rec, err);
-            cursor_accumulate(A, S, ja, sa, dxa, dya, dza, fx.scale);
-            if (bact) cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale);
+        // ---- 3. the warp's compacted owner table: one packed scan (owners | entries << 8)
+        const int v = (cnt > 0 ? 1 : 0) | (cnt << 8);
+        const int incl = warp_incl_scan(v, lane);
+        const int tp = __shfl_sync(0xffffffffu, incl, 31);
+        const int nown = tp & 0xFF, tot = tp >> 8;
+        if (cnt > 0) {
+            const int o = (incl - v) & 0xFF, e = (incl - v) >> 8;
+            S.woex[wb + o] = e;
+            S.wsi[wb + o] = s_i;
+            S.wrow[wb + o] = tid * FT_LSTRIDE - e;
         }
-        cursor_flush(A, S);
-        cursor_flush(B, S);
+        if (lane == 0) S.woex[wb + nown] = tot;
+        __syncwarp();
+
+        // ---- 4. pair evaluation: contiguous chunk of the warp's lists per lane, walked by two
+        //         independent cursors (halves of the chunk) so two Philox/Box-Muller chains
+        //         are in flight per thread (instruction-level parallelism)
+        if (tot > 0) {
+            const int C = (tot + 31) >> 5;
+            const int t0 = min(lane * C, tot);
+            const int t1 = min(t0 + C, tot);
+            const int tm = t0 + ((t1 - t0 + 1) >> 1);
+            PairCursor A, B;
+            cursor_init(A, S, t0, tm, wb, nown);
+            cursor_init(B, S, tm, t1, wb, nown);
+            while (A.t < A.t1) { // B is never longer than A
+                const int ja = cursor_next(A, S);
+                const bool bact = B.t < B.t1;
+                const int jb = bact ? cursor_next(B, S) : B.si; // inactive: self pair, r2 = 0 -> f = 0
+                float dxa, dya, dza, dxb, dyb, dzb;
+                const float sa = pair_core<KMODE>(pp, A.pi, A.vi, S.sp[ja], S.sv[ja], ks, dxa, dya, dza);
+                const float sb = pair_core<KMODE>(pp, B.pi, B.vi, S.sp[jb], S.sv[jb], ks, dxb, dyb, dzb);
+                pair_checks<RECORD>(pp, fx, A.pi, S.sp[ja], sa, dxa, dya, dza, ks, rec, err);
+                if (bact) pair_checks<RECORD>(pp, fx, B.pi, S.sp[jb], sb, dxb, dyb, dzb, ks, rec, err);
+                cursor_accumulate(A, S, ja, sa, dxa, dya, dza, fx.scale);
+                if (bact) cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale);
+            }
+            cursor_flush(A, S);
+            cursor_flush(B, S);
+        }
+        __syncwarp(); // the lists and the owner table are rewritten by the next round
     }
     __syncthreads();
 
@@ -603,7 +649,6 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int c0 = sxa * row;
         const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
-        const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
         const int gm = wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0];
         for (int s = a0 + lane; s < e0; s += 32) {
