@@ -74,13 +74,21 @@ int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
 /* Engine options (name, value):
  *   "force_kernel" 0 = tiled shared-memory kernel with fixed-point accumulation (default,
  *                  DESIGN.md §6), 1 = reference thread-per-particle kernel with fp32
- *                  global atomics (P:276-278 mapping; kept as a cross-check).
- * Unknown names -> DPD_ERR_ARG. */
+ *                  global atomics (P:276-278 mapping; kept as a cross-check), 2 = cell-warp
+ *                  variant of the tiled kernel (one warp per home cell; same results up
+ *                  to fp32 summation order).  1 and 2 are single-domain only.
+ *   "message_capacity_percent" (distributed contexts) scales the per-direction message
+ *                  capacities (default 100; >= 10).
+ * Out-of-range values -> DPD_ERR_ARG; unknown names -> DPD_ERR_ARG. */
 int dpd_set_option(dpd_ctx *ctx, const char *name, int64_t value);
 
-/* Engine statistics (cumulative since creation): "fallback_tiles" = tiles of the tiled
- * force kernel that exceeded a shared-memory capacity and were evaluated by its global-memory
- * fallback ("fallback_staged", "fallback_home", "fallback_list" split it by cause). */
+/* Engine statistics (cumulative since creation), name -> *value:
+ *   "fallback_tiles"      tiles of the tiled force kernel that exceeded a shared-memory
+ *                         capacity and were evaluated by its global-memory fallback;
+ *   "fallback_staged", "fallback_home"  the same split by cause (staged / home capacity);
+ *   "full_list_particles" home particles whose pair list filled up, so that the rest of
+ *                         their candidates were evaluated in place (still exact).
+ * Unknown names -> DPD_ERR_ARG. */
 int dpd_get_stat(dpd_ctx *ctx, const char *name, int64_t *value);
 
 /* Periodic-Poiseuille body force: f_body = (0,0,-f) for r_x <= L_x/2 and

@@ -103,7 +103,7 @@ struct dpd_ctx {
     uint64_t seed;
     double body_f = 0.0;
     int kmode = 2;
-    int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel
+    int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel, 2: cell-warp
     Geom geom{};
     PairP pp{};
     FixP fix{};
@@ -955,7 +955,7 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
     if (strcmp(name, "force_kernel") == 0) {
         if (value < 0 || value > 2)
             return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled), 1 (reference) or 2 (cell-warp)");
-        if (value == 1 && c->dist) return fail(c, DPD_ERR_ARG, "the reference kernel is single-domain only");
+        if (value != 0 && c->dist) return fail(c, DPD_ERR_ARG, "force_kernel %d is single-domain only", (int)value);
         c->force_impl = (int)value;
         return DPD_OK;
     }

@@ -29,7 +29,7 @@ constexpr int FT_BX = 4, FT_BY = 4, FT_BZ = 2;
 constexpr int FT_SX = FT_BX + 2, FT_SY = FT_BY + 2, FT_SZ = FT_BZ + 1;
 constexpr int FT_NSC = FT_SX * FT_SY * FT_SZ; // staged cells (108)
 constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
-constexpr int FT_NTHR = 288;                  // > mean home count (256)
+constexpr int FT_NTHR = 288;                  // 9 warps: ~28 home particles each (balanced ranges)
 constexpr int FT_NWARP = FT_NTHR / 32;
 constexpr int FT_SCAP = 1152;                 // staged particles (mean 864, sd 29 at rho = 8)
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
@@ -48,7 +48,7 @@ struct FixP {
 struct ForceTileSmem {
     float4 sp[FT_SCAP];                          // staged positions (tile frame), w = id bits
     float4 sv[FT_SCAP];                          // staged velocities
-    float sx[FT_SCAP + 4], sy[FT_SCAP + 4], sz[FT_SCAP + 4]; // SoA positions (sweep; +4: masked over-reads)
+    float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // SoA copy of the positions for the sweep
     int acc[3][FT_SCAP];                         // fixed-point force sums
     unsigned short lst[FT_NTHR * FT_LSTRIDE];    // per-thread pair lists (one home particle each)
     int woex[FT_NWARP * FT_WSTRIDE];             // per warp: compacted owners' list prefix (+ total)
@@ -88,16 +88,6 @@ __device__ __forceinline__ void append_if(unsigned &lptr, float r2, float rc2, u
                  "@p add.u32 %0, %0, 2;\n\t}"
                  : "+r"(lptr)
                  : "f"(r2), "f"(rc2), "r"(j)
-                 : "memory");
-}
-
-// Append j if r2 < rc2 and j < hi (candidate masking at a segment's end).
-__device__ __forceinline__ void append_if_below(unsigned &lptr, float r2, float rc2, unsigned j, unsigned hi)
-{
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tsetp.lt.and.u32 p, %3, %4, p;\n\t"
-                 "@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
-                 : "+r"(lptr)
-                 : "f"(r2), "f"(rc2), "r"(j), "r"(hi)
                  : "memory");
 }
 
