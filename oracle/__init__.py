@@ -35,7 +35,9 @@ class Params(C.Structure):
     """Mirror of ``oracle_params`` in dpd_oracle.c."""
     _fields_ = [("box", C.c_double * 3), ("rc", C.c_double), ("a", C.c_double),
                 ("gamma", C.c_double), ("kT", C.c_double), ("power", C.c_double),
-                ("dt", C.c_double), ("seed", C.c_uint64), ("body_f", C.c_double)]
+                ("dt", C.c_double), ("seed", C.c_uint64), ("body_f", C.c_double),
+                ("nspecies", C.c_int32), ("amat", C.c_double * 16), ("gmat", C.c_double * 16),
+                ("species", C.POINTER(C.c_int32))]
 
 
 @dataclass
@@ -49,6 +51,11 @@ class DPDParams:
     dt: float = 0.01
     seed: int = 42
     body_f: float = 0.0
+    # NEXT-2 species matrices (ns x ns, symmetric) and per-particle species (index order);
+    # None = single species (a, gamma)
+    amat: object = None
+    gmat: object = None
+    species: object = None
 
     def c(self) -> Params:
         p = Params()
@@ -56,6 +63,20 @@ class DPDParams:
             p.box[k] = float(self.box[k])
         p.rc, p.a, p.gamma, p.kT = float(self.rc), float(self.a), float(self.gamma), float(self.kT)
         p.power, p.dt, p.seed, p.body_f = float(self.power), float(self.dt), int(self.seed), float(self.body_f)
+        if self.amat is not None:
+            A = np.asarray(self.amat, np.float64)
+            G = np.asarray(self.gmat, np.float64)
+            ns = A.shape[0]
+            if A.shape != (ns, ns) or G.shape != (ns, ns) or ns > 4:
+                raise ValueError("species matrices must be square, equal, <= 4 x 4")
+            p.nspecies = ns
+            for k, val in enumerate(A.ravel()):
+                p.amat[k] = float(val)
+            for k, val in enumerate(G.ravel()):
+                p.gmat[k] = float(val)
+            if self.species is not None:
+                self._sp = np.ascontiguousarray(self.species, np.int32)  # kept alive with p
+                p.species = self._sp.ctypes.data_as(C.POINTER(C.c_int32))
         return p
 
 

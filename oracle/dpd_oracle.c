@@ -19,6 +19,7 @@
  *   - Groot-Warren velocity Verlet, lambda = 1/2 ("fused VV")            (C-6)
  *   - observables: kinetic T (full-step v), conservative virial p       (C-14, C-15)
  *   - an fp64 cell-list sweep (CPU timing mode, never used as truth)    (C-2 item 7)
+ *   - per-pair (a, gamma) from a species matrix
  *
  * Parity pins: see tests/test_oracle_*.py (Random123 KATs, hand examples S:194/S:196,
  * closed forms, invariants, brute force vs cell list, T = kT, Groot-Warren EOS).
@@ -42,7 +43,25 @@ typedef struct {
     double dt;      /* time step                                             (C-3)       */
     uint64_t seed;  /* Philox key                                            (C-7)       */
     double body_f;  /* periodic-Poiseuille body force magnitude f */
+    /* Species interaction matrix: with nspecies > 1 and a
+     * species array, the pair (i, j) uses a = amat[s_i][s_j], gamma = gmat[s_i][s_j] and
+     * sigma = sqrt(2 gamma kT) (per pair) in place of a, gamma above.            */
+    int32_t nspecies;        /* 0 or 1: single species                                */
+    double amat[16];         /* nspecies x nspecies, row-major (nspecies <= 4)        */
+    double gmat[16];
+    const int32_t *species;  /* species of particle index i (NULL: all 0)             */
 } oracle_params;
+
+/* The parameters of pair (i, j): p itself, or a copy with the pair's (a, gamma). */
+static const oracle_params *pair_params(const oracle_params *p, int64_t i, int64_t j, oracle_params *q)
+{
+    if (p->nspecies <= 1 || !p->species) return p;
+    *q = *p;
+    const int32_t ns = p->nspecies, si = p->species[i], sj = p->species[j];
+    q->a = p->amat[si * ns + sj];
+    q->gamma = p->gmat[si * ns + sj];
+    return q;
+}
 
 /* ------------------------------------------------------------------------------------
  * Philox4x32-10 (Salmon et al., SC'11 "Random123"), as fixed by reading C-7.
@@ -195,9 +214,11 @@ int oracle_forces(const oracle_params *p, int64_t n, const double *x, const doub
         for (int64_t j = 0; j < n; ++j) {
             if (j == i) continue;
             double d[3], vij[3], f[3], xi = 0.0;
+            oracle_params q;
+            const oracle_params *pp = pair_params(p, i, j, &q);
             oracle_min_image(p, &x[3 * i], &x[3 * j], d);
             for (int k = 0; k < 3; ++k) vij[k] = v[3 * i + k] - v[3 * j + k];
-            int hit = oracle_pair_force(p, d, vij, ids[i], ids[j], step, f, &xi);
+            int hit = oracle_pair_force(pp, d, vij, ids[i], ids[j], step, f, &xi);
             if (hit) {
                 Fi[0] += f[0]; Fi[1] += f[1]; Fi[2] += f[2];
                 if (j > i) count += 1;
@@ -210,7 +231,7 @@ int oracle_forces(const oracle_params *p, int64_t n, const double *x, const doub
                         oracle_pair_words(p->seed, step, ids[i], ids[j], wds);
                         xi = oracle_xi(wds[0], wds[1]);
                     }
-                    al += boundary_bound(p, eps, vij, xi);
+                    al += boundary_bound(pp, eps, vij, xi);
                 }
             }
         }
@@ -242,7 +263,9 @@ int oracle_forces_subset(const oracle_params *p, int64_t n, const double *x, con
             double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
             if (r2 >= (p->rc + eps) * (p->rc + eps)) continue; /* no force, not a boundary pair */
             for (int c = 0; c < 3; ++c) vij[c] = v[3 * i + c] - v[3 * j + c];
-            int hit = oracle_pair_force(p, d, vij, ids[i], ids[j], step, f, &xi);
+            oracle_params q;
+            const oracle_params *pp = pair_params(p, i, j, &q);
+            int hit = oracle_pair_force(pp, d, vij, ids[i], ids[j], step, f, &xi);
             if (hit) { Fi[0] += f[0]; Fi[1] += f[1]; Fi[2] += f[2]; }
             double r = sqrt(r2);
             if (fabs(r - p->rc) < eps) {
@@ -251,7 +274,7 @@ int oracle_forces_subset(const oracle_params *p, int64_t n, const double *x, con
                     oracle_pair_words(p->seed, step, ids[i], ids[j], wds);
                     xi = oracle_xi(wds[0], wds[1]);
                 }
-                al += boundary_bound(p, eps, vij, xi);
+                al += boundary_bound(pp, eps, vij, xi);
             }
         }
         F[3 * k + 0] = Fi[0];
@@ -416,7 +439,7 @@ double oracle_temperature(int64_t n, const double *v)
 }
 
 /* Conservative virial sum W = sum_{i<j} a w(r) r (C-2 item 6), so that
- * p = rho T + W / (3 V).  Brute force, minimum image. */
+ * p = rho T + W / (3 V).  Brute force, minimum image; single species (uses p->a). */
 double oracle_virial(const oracle_params *p, int64_t n, const double *x)
 {
     double W = 0.0;
@@ -489,7 +512,8 @@ int oracle_forces_celllist(const oracle_params *p, int64_t n, const double *x, c
                         double d[3], vij[3], f[3];
                         oracle_min_image(p, &x[3 * i], &x[3 * j], d);
                         for (int k = 0; k < 3; ++k) vij[k] = v[3 * i + k] - v[3 * j + k];
-                        if (oracle_pair_force(p, d, vij, ids[i], ids[j], step, f, NULL)) {
+                        oracle_params q;
+                        if (oracle_pair_force(pair_params(p, i, j, &q), d, vij, ids[i], ids[j], step, f, NULL)) {
                             Fi[0] += f[0]; Fi[1] += f[1]; Fi[2] += f[2];
                             if (j > i) count += 1;
                         }
