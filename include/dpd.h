@@ -91,6 +91,18 @@ int dpd_set_option(dpd_ctx *ctx, const char *name, int64_t value);
  * Unknown names -> DPD_ERR_ARG. */
 int dpd_get_stat(dpd_ctx *ctx, const char *name, int64_t *value);
 
+/* Species interaction matrix (fluids of different
+ * viscosity, conservative-only or viscous-only cross interactions are per-pair choices of
+ * a and gamma).  a and gamma are nspecies x nspecies row-major, symmetric, finite, >= 0;
+ * the pair of species (s_i, s_j) interacts with a_{s_i s_j}, gamma_{s_i s_j} and
+ * sigma_{s_i s_j} = sqrt(2 gamma_{s_i s_j} kT) (fluctuation-dissipation per pair);
+ * r_c, kT and k stay global.  1 <= nspecies <= 4.  Must precede dpd_set_particles*
+ * (DPD_ERR_ARG otherwise).  nspecies = 1 replaces (a, gamma) of dpd_create.  Species of
+ * each particle are given to dpd_set_particles_typed (default 0) and travel with it
+ * through migration and ghost exchange.  Errors: DPD_ERR_ARG, DPD_ERR_CONFIG (negative,
+ * non-finite or asymmetric entries). */
+int dpd_set_species(dpd_ctx *ctx, int nspecies, const double *a, const double *gamma);
+
 /* Periodic-Poiseuille body force: f_body = (0,0,-f) for r_x <= L_x/2 and
  * (0,0,+f) otherwise (global coordinates).  f = 0 (default) disables it.  The body force
  * enters the integrator, not dpd_get_forces. */
@@ -108,6 +120,11 @@ int dpd_set_particles(dpd_ctx *ctx, int64_t n, const float *pos, const float *ve
  * subdomain.  ids may be NULL (ids := 0..n-1). */
 int dpd_set_particles_ex(dpd_ctx *ctx, int64_t n, const float *pos, const float *vel,
                          const int32_t *ids, int64_t step0);
+
+/* As dpd_set_particles_ex with a species index per particle (species may be NULL: all
+ * 0).  An index outside [0, nspecies) is reported as DPD_ERR_ARG by this call. */
+int dpd_set_particles_typed(dpd_ctx *ctx, int64_t n, const float *pos, const float *vel,
+                            const int32_t *ids, const int32_t *species, int64_t step0);
 
 /* Advance nsteps >= 0 steps of Groot-Warren VV (C-2 item 3):
  *   u = v + dt/2 (F + f_body);  x = wrap(x + dt u);  s += 1;  rebuild cells;
@@ -205,6 +222,14 @@ int dpd_get_particles_ex(dpd_ctx *ctx, int64_t cap, float *pos, float *vel, int3
 
 /* Forces of the local particles in storage order (same order as dpd_get_particles_ex). */
 int dpd_get_forces_ex(dpd_ctx *ctx, int64_t cap, float *f, int32_t *ids, int64_t *n);
+
+/* Species index of every particle (NEXT-2), row id of species[n] (dense ids required, as
+ * dpd_get_particles). */
+int dpd_get_species(dpd_ctx *ctx, int64_t n, int32_t *species);
+
+/* Species of the local particles in storage order (same order as dpd_get_particles_ex);
+ * ids (may be NULL) receives the matching ids, *n the count; cap < count -> DPD_ERR_ARG. */
+int dpd_get_species_ex(dpd_ctx *ctx, int64_t cap, int32_t *species, int32_t *ids, int64_t *n);
 
 /* ---- debug / parity hooks (T0: device RNG against the Random123 known answers) ------- */
 

@@ -41,6 +41,8 @@ SIGNATURES = [
     ("dpd_get_stat", C.c_int, [_vp, C.c_char_p, _P(C.c_int64)]),
     ("dpd_set_particles", C.c_int, [_vp, C.c_int64, _vp, _vp]),
     ("dpd_set_particles_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, C.c_int64]),
+    ("dpd_set_particles_typed", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, C.c_int64]),
+    ("dpd_set_species", C.c_int, [_vp, C.c_int, _P(C.c_double), _P(C.c_double)]),
     ("dpd_step", C.c_int, [_vp, C.c_int64]),
     ("dpd_step_async", C.c_int, [_vp, C.c_int64]),
     ("dpd_sync", C.c_int, [_vp]),
@@ -65,6 +67,8 @@ SIGNATURES = [
     ("dpd_group_step", C.c_int, [_P(_vp), C.c_int, C.c_int64]),
     ("dpd_get_particles_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _P(C.c_int64)]),
     ("dpd_get_forces_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _P(C.c_int64)]),
+    ("dpd_get_species", C.c_int, [_vp, C.c_int64, _vp]),
+    ("dpd_get_species_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _P(C.c_int64)]),
     ("dpd_debug_philox", C.c_int, [C.c_int64, _vp, _vp, _vp]),
     ("dpd_debug_pair_words", C.c_int, [C.c_int64, _vp, C.c_uint64, _vp, _vp]),
 ]
@@ -149,6 +153,22 @@ def dpd_set_particles(ctx, pos, vel):
 def dpd_set_particles_ex(ctx, pos, vel, ids=None, step0=0):
     n = int(pos.shape[0])
     _check(ctx, load().dpd_set_particles_ex(ctx, n, _ptr(pos), _ptr(vel), _ptr(ids), int(step0)))
+
+
+def dpd_set_particles_typed(ctx, pos, vel, ids=None, species=None, step0=0):
+    n = int(pos.shape[0])
+    _check(ctx, load().dpd_set_particles_typed(ctx, n, _ptr(pos), _ptr(vel), _ptr(ids), _ptr(species), int(step0)))
+
+
+def dpd_set_species(ctx, a, gamma):
+    """a, gamma: nspecies x nspecies symmetric matrices (NEXT-2)."""
+    a = np.ascontiguousarray(a, np.float64)
+    gamma = np.ascontiguousarray(gamma, np.float64)
+    ns = int(a.shape[0])
+    if a.shape != (ns, ns) or gamma.shape != (ns, ns):
+        raise ValueError("a and gamma must be square and of equal size")
+    _check(ctx, load().dpd_set_species(ctx, ns, a.ctypes.data_as(_P(C.c_double)),
+                                       gamma.ctypes.data_as(_P(C.c_double))))
 
 
 def dpd_step(ctx, nsteps):
@@ -358,6 +378,24 @@ def dpd_get_forces_ex(ctx, f=None, ids=None):
     cnt = C.c_int64()
     _check(ctx, load().dpd_get_forces_ex(ctx, int(f.shape[0]), _ptr(f), _ptr(ids), C.byref(cnt)))
     return f[: cnt.value], ids[: cnt.value]
+
+
+def dpd_get_species(ctx, out=None):
+    """Species index per particle in id order (dense ids)."""
+    n = dpd_get_count(ctx)
+    out = np.empty(n, np.int32) if out is None else out
+    _check(ctx, load().dpd_get_species(ctx, n, _ptr(out)))
+    return out
+
+
+def dpd_get_species_ex(ctx, species=None, ids=None):
+    """Species and ids of the local particles in storage order."""
+    n = dpd_get_count(ctx)
+    species = np.empty(n, np.int32) if species is None else species
+    ids = np.empty(n, np.int32) if ids is None else ids
+    cnt = C.c_int64()
+    _check(ctx, load().dpd_get_species_ex(ctx, int(species.shape[0]), _ptr(species), _ptr(ids), C.byref(cnt)))
+    return species[: cnt.value], ids[: cnt.value]
 
 
 def dpd_plan_peers(grid, rank):

@@ -103,6 +103,7 @@ struct dpd_ctx {
     uint64_t seed;
     double body_f = 0.0;
     int kmode = 2;
+    int nspecies = 1;   // NEXT-2 species matrix size (kmode 3 when > 1)
     int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel, 2: cell-warp
     Geom geom{};
     PairP pp{};
@@ -265,6 +266,8 @@ int sync_check(dpd_ctx *c)
                         (long long)c->step);
         if (flags & ERR_CAPACITY)
             return fail(c, DPD_ERR_CAPACITY, "device buffer capacity exceeded (particles, ghosts or migrants)");
+        if (flags & ERR_SPECIES)
+            return fail(c, DPD_ERR_ARG, "species index out of range (particle id %d; %d species)", id, c->nspecies);
         if (flags & ERR_RANGE)
             return fail(c, DPD_ERR_NUMERIC,
                         "particle id %d moved more than one (sub)domain in a step or a pair force left the "
@@ -395,13 +398,15 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
                 switch (c->kmode) {
                 case 0: DPD_CELLS(true, 0); break;
                 case 1: DPD_CELLS(true, 1); break;
-                default: DPD_CELLS(true, 2); break;
+                case 2: DPD_CELLS(true, 2); break;
+                default: DPD_CELLS(true, 3); break;
                 }
             } else {
                 switch (c->kmode) {
                 case 0: DPD_CELLS(false, 0); break;
                 case 1: DPD_CELLS(false, 1); break;
-                default: DPD_CELLS(false, 2); break;
+                case 2: DPD_CELLS(false, 2); break;
+                default: DPD_CELLS(false, 3); break;
                 }
             }
 #undef DPD_CELLS
@@ -421,13 +426,15 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;
                 case 1: DPD_TILE(true, 1); break;
-                default: DPD_TILE(true, 2); break;
+                case 2: DPD_TILE(true, 2); break;
+                default: DPD_TILE(true, 3); break;
                 }
             } else {
                 switch (c->kmode) {
                 case 0: DPD_TILE(false, 0); break;
                 case 1: DPD_TILE(false, 1); break;
-                default: DPD_TILE(false, 2); break;
+                case 2: DPD_TILE(false, 2); break;
+                default: DPD_TILE(false, 3); break;
                 }
             }
 #undef DPD_TILE
@@ -444,13 +451,15 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
             switch (c->kmode) {
             case 0: DPD_REF(true, 0); break;
             case 1: DPD_REF(true, 1); break;
-            default: DPD_REF(true, 2); break;
+            case 2: DPD_REF(true, 2); break;
+            default: DPD_REF(true, 3); break;
             }
         } else {
             switch (c->kmode) {
             case 0: DPD_REF(false, 0); break;
             case 1: DPD_REF(false, 1); break;
-            default: DPD_REF(false, 2); break;
+            case 2: DPD_REF(false, 2); break;
+            default: DPD_REF(false, 3); break;
             }
         }
 #undef DPD_REF
@@ -483,7 +492,8 @@ int phase_halo(dpd_ctx *c, int64_t step)
         switch (c->kmode) {
         case 0: k_force_halo<0><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
         case 1: k_force_halo<1><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
-        default: k_force_halo<2><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
+        case 2: k_force_halo<2><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
+        default: k_force_halo<3><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
         }
     });
 }
@@ -713,6 +723,25 @@ int setup_geometry(dpd_ctx *c, const double len[3], const int split[3])
     return DPD_OK;
 }
 
+// Fixed-point scale of the tiled kernel for the largest pair amplitudes a and
+// gamma in use: bound a single pair's force magnitude by a + 6.7 sigma/sqrt(dt) (|xi| <= 6.66
+// with 32-bit u1) + 20 gamma max(1, sqrt(kT)) (relative speed), keep |f scale| < 2^21;
+// larger magnitudes are detected on the device and reported as DPD_ERR_NUMERIC.
+void set_fixed_scale(dpd_ctx *c, double amax, double gmax)
+{
+    const double sig_dt = std::sqrt(2.0 * gmax * c->kT) / std::sqrt(c->dt);
+    const double bound = amax + 6.7 * sig_dt + 20.0 * gmax * std::max(1.0, std::sqrt(c->kT)) + 1e-30;
+    int k = (int)std::floor(std::log2(std::ldexp(1.0, 21) / bound));
+    k = std::min(20, std::max(-20, k));
+    c->fix.scale = (float)std::ldexp(1.0, k);
+    c->fix.inv_scale = (float)std::ldexp(1.0, -k);
+    c->fix.mag_lim = (float)std::ldexp(1.0, 21 - k);
+    // row-end pruning slack: far above the cell-binning rounding of
+    // coordinates up to the box extent, far below any cell size
+    const double lmax = std::max(c->box[0], std::max(c->box[1], c->box[2]));
+    c->fix.slack = (float)(1e-4 + lmax * std::ldexp(1.0, -20));
+}
+
 int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma, double kT, double power, double dt,
              uint64_t seed)
 {
@@ -727,46 +756,36 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     c->seed = seed;
     c->kmode = (power == 0.5) ? 0 : (power == 1.0 ? 1 : 2);
     for (int d = 0; d < 27; ++d) c->peer_to[d] = c->peer_from[d] = -1;
-    PairP pp;
+    PairP pp{};
     pp.a = (float)a;
     pp.gamma = (float)gamma;
     pp.sig_dt = (float)(std::sqrt(2.0 * gamma * kT) / std::sqrt(dt));
+    pp.sa[0] = pp.a; // one species until dpd_set_species
+    pp.sg[0] = pp.gamma;
+    pp.ss[0] = pp.sig_dt;
     pp.inv_rc = (float)(1.0 / rc);
     pp.rc2 = (float)(rc * rc);
     pp.power = (float)power;
     pp.seed_fold = (uint32_t)seed ^ (uint32_t)(seed >> 32);
     c->pp = pp;
-    // Fixed-point scale of the tiled kernel: bound a single pair's force
-    // magnitude by a + 6.7 sigma/sqrt(dt) (|xi| <= 6.66 with 32-bit u1) + 20 gamma
-    // max(1, sqrt(kT)) (relative speed), keep |f scale| < 2^21; larger magnitudes are
-    // detected on the device and reported as DPD_ERR_NUMERIC.
-    {
-        const double bound = a + 6.7 * (double)pp.sig_dt + 20.0 * gamma * std::max(1.0, std::sqrt(kT)) + 1e-30;
-        int k = (int)std::floor(std::log2(std::ldexp(1.0, 21) / bound));
-        k = std::min(20, std::max(-20, k));
-        c->fix.scale = (float)std::ldexp(1.0, k);
-        c->fix.inv_scale = (float)std::ldexp(1.0, -k);
-        c->fix.mag_lim = (float)std::ldexp(1.0, 21 - k);
-        // row-end pruning slack: far above the cell-binning rounding of
-        // coordinates up to the box extent, far below any cell size
-        const double lmax = std::max(box[0], std::max(box[1], box[2]));
-        c->fix.slack = (float)(1e-4 + lmax * std::ldexp(1.0, -20));
-    }
+    set_fixed_scale(c, a, gamma);
     {
         // two tiles per SM need the maximum shared-memory carveout (2 x (smem + 1 KB) <= 228 KB)
         const int smem = (int)sizeof(ForceTileSmem);
-        const void *fns[6] = {(const void *)k_force_tile<false, 0>, (const void *)k_force_tile<false, 1>,
-                              (const void *)k_force_tile<false, 2>, (const void *)k_force_tile<true, 0>,
-                              (const void *)k_force_tile<true, 1>,  (const void *)k_force_tile<true, 2>};
+        const void *fns[8] = {(const void *)k_force_tile<false, 0>, (const void *)k_force_tile<false, 1>,
+                              (const void *)k_force_tile<false, 2>, (const void *)k_force_tile<false, 3>,
+                              (const void *)k_force_tile<true, 0>,  (const void *)k_force_tile<true, 1>,
+                              (const void *)k_force_tile<true, 2>,  (const void *)k_force_tile<true, 3>};
         for (const void *f : fns) {
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxShared));
         }
         const int smc = (int)sizeof(ForceCellSmem);
-        const void *fcs[6] = {(const void *)k_force_cells<false, 0>, (const void *)k_force_cells<false, 1>,
-                              (const void *)k_force_cells<false, 2>, (const void *)k_force_cells<true, 0>,
-                              (const void *)k_force_cells<true, 1>,  (const void *)k_force_cells<true, 2>};
+        const void *fcs[8] = {(const void *)k_force_cells<false, 0>, (const void *)k_force_cells<false, 1>,
+                              (const void *)k_force_cells<false, 2>, (const void *)k_force_cells<false, 3>,
+                              (const void *)k_force_cells<true, 0>,  (const void *)k_force_cells<true, 1>,
+                              (const void *)k_force_cells<true, 2>,  (const void *)k_force_cells<true, 3>};
         for (const void *f : fcs) {
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smc));
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -982,6 +1001,48 @@ int dpd_get_stat(dpd_ctx *c, const char *name, int64_t *value)
     return fail(c, DPD_ERR_ARG, "unknown statistic '%s'", name);
 }
 
+int dpd_set_species(dpd_ctx *c, int nspecies, const double *a, const double *gamma)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (nspecies < 1 || nspecies > DPD_MAX_SPECIES)
+        return fail(c, DPD_ERR_ARG, "nspecies must be in [1, %d]", DPD_MAX_SPECIES);
+    if (!a || !gamma) return fail(c, DPD_ERR_ARG, "null species matrix");
+    if (c->primed) return fail(c, DPD_ERR_ARG, "dpd_set_species must precede dpd_set_particles*");
+    const int ns = nspecies;
+    double amax = 0.0, gmax = 0.0;
+    for (int i = 0; i < ns; ++i)
+        for (int j = 0; j < ns; ++j) {
+            const double av = a[i * ns + j], gv = gamma[i * ns + j];
+            if (!std::isfinite(av) || !std::isfinite(gv) || av < 0.0 || gv < 0.0)
+                return fail(c, DPD_ERR_CONFIG, "species matrix entries must be finite and >= 0");
+            if (av != a[j * ns + i] || gv != gamma[j * ns + i])
+                return fail(c, DPD_ERR_CONFIG, "species matrices must be symmetric (Newton-3 pairs)");
+            amax = std::max(amax, av);
+            gmax = std::max(gmax, gv);
+        }
+    PairP &pp = c->pp;
+    for (int t = 0; t < DPD_MAX_SPECIES * DPD_MAX_SPECIES; ++t) pp.sa[t] = pp.sg[t] = pp.ss[t] = 0.0f;
+    for (int i = 0; i < ns; ++i)
+        for (int j = 0; j < ns; ++j) {
+            const int t = i * DPD_MAX_SPECIES + j;
+            const double gv = gamma[i * ns + j];
+            pp.sa[t] = (float)a[i * ns + j];
+            pp.sg[t] = (float)gv;
+            pp.ss[t] = (float)(std::sqrt(2.0 * gv * c->kT) / std::sqrt(c->dt)); // FDT per pair
+        }
+    if (ns == 1) {
+        c->a = a[0];
+        c->gamma = gamma[0];
+        pp.a = (float)a[0];
+        pp.gamma = (float)gamma[0];
+        pp.sig_dt = pp.ss[0];
+    }
+    c->nspecies = ns;
+    c->kmode = (ns > 1) ? 3 : ((c->power == 0.5) ? 0 : (c->power == 1.0 ? 1 : 2));
+    set_fixed_scale(c, amax, gmax);
+    return DPD_OK;
+}
+
 int dpd_set_body_force(dpd_ctx *c, double f)
 {
     if (!c) return DPD_ERR_ARG;
@@ -991,6 +1052,12 @@ int dpd_set_body_force(dpd_ctx *c, double f)
 }
 
 int dpd_set_particles_ex(dpd_ctx *c, int64_t n, const float *pos, const float *vel, const int32_t *ids, int64_t step0)
+{
+    return dpd_set_particles_typed(c, n, pos, vel, ids, nullptr, step0);
+}
+
+int dpd_set_particles_typed(dpd_ctx *c, int64_t n, const float *pos, const float *vel, const int32_t *ids,
+                            const int32_t *species, int64_t step0)
 {
     if (!c) return DPD_ERR_ARG;
     if (n < 0 || n > (int64_t)INT32_MAX / 2) return fail(c, DPD_ERR_ARG, "bad particle count %lld", (long long)n);
@@ -1012,10 +1079,11 @@ int dpd_set_particles_ex(dpd_ctx *c, int64_t n, const float *pos, const float *v
     c->step = step0;
     c->cur = 0;
     c->scur = 0;
-    const size_t words = (size_t)std::max<int64_t>(n, 1) * 7;
+    const size_t words = (size_t)std::max<int64_t>(n, 1) * 8;
     CUDA_TRY(c, c->stage.reserve(words));
     float *d_pos = c->stage.p, *d_vel = c->stage.p + 3 * (size_t)n;
     int32_t *d_ids = ids ? reinterpret_cast<int32_t *>(c->stage.p + 6 * (size_t)n) : nullptr;
+    int32_t *d_species = species ? reinterpret_cast<int32_t *>(c->stage.p + 7 * (size_t)n) : nullptr;
     int *n_out = count_ptr(c);
     const float3 gbox = make_float3((float)c->box[0], (float)c->box[1], (float)c->box[2]);
     const float3 org = make_float3(c->origin[0], c->origin[1], c->origin[2]);
@@ -1024,6 +1092,8 @@ int dpd_set_particles_ex(dpd_ctx *c, int64_t n, const float *pos, const float *v
         CUDA_TRY(c, cudaMemcpyAsync(d_pos, pos, sizeof(float) * 3 * n, cudaMemcpyDefault, c->stream));
         CUDA_TRY(c, cudaMemcpyAsync(d_vel, vel, sizeof(float) * 3 * n, cudaMemcpyDefault, c->stream));
         if (ids) CUDA_TRY(c, cudaMemcpyAsync(d_ids, ids, sizeof(int32_t) * n, cudaMemcpyDefault, c->stream));
+        if (species)
+            CUDA_TRY(c, cudaMemcpyAsync(d_species, species, sizeof(int32_t) * n, cudaMemcpyDefault, c->stream));
     }
     // particle arrays: exactly n on one domain; decomposed runs count the particles inside the
     // subdomain first and leave room for migration fluctuations
@@ -1044,8 +1114,9 @@ int dpd_set_particles_ex(dpd_ctx *c, int64_t n, const float *pos, const float *v
         const Geom g = c->geom;
         const int cap = (int)c->n_cap;
         TRY(launch(c, KID_PACK, [&] {
-            k_pack_input<<<nblk(n, 256), 256, 0, c->stream>>>(d_pos, d_vel, d_ids, n, g, gbox, org, c->pos[0].p,
-                                                              c->vel[0].p, c->frc[0].p, n_out, cap, c->err.p);
+            k_pack_input<<<nblk(n, 256), 256, 0, c->stream>>>(d_pos, d_vel, d_ids, d_species, c->nspecies, n, g,
+                                                              gbox, org, c->pos[0].p, c->vel[0].p, c->frc[0].p,
+                                                              n_out, cap, c->err.p);
         }));
     }
     TRY(sync_check(c)); // local count (capacity errors surface here)
@@ -1462,6 +1533,39 @@ int dpd_get_particles_ex(dpd_ctx *c, int64_t cap, float *pos, float *vel, int32_
     if (n) *n = c->n;
     if (cap < c->n) return fail(c, DPD_ERR_ARG, "cap %lld < count %lld", (long long)cap, (long long)c->n);
     TRY(gather(c, pos, vel, nullptr, 0));
+    return copy_ids(c, ids);
+}
+
+static int species_out(dpd_ctx *c, int32_t *species, int by_id)
+{
+    if (!species || c->n == 0) return DPD_OK;
+    CUDA_TRY(c, c->stage.reserve((size_t)c->n));
+    int32_t *d = reinterpret_cast<int32_t *>(c->stage.p);
+    const int b = c->cur;
+    TRY(launch(c, KID_GATHER, [&] {
+        k_species_out<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, (int)c->n, d, by_id);
+    }));
+    CUDA_TRY(c, cudaMemcpyAsync(species, d, sizeof(int32_t) * c->n, cudaMemcpyDefault, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return DPD_OK;
+}
+
+int dpd_get_species(dpd_ctx *c, int64_t n, int32_t *species)
+{
+    if (!c) return DPD_ERR_ARG;
+    TRY(sync_check(c));
+    if (n != c->n) return fail(c, DPD_ERR_ARG, "n = %lld but the context holds %lld", (long long)n, (long long)c->n);
+    if (!c->dense_ids) return fail(c, DPD_ERR_ARG, "ids are not dense 0..n-1; use dpd_get_species_ex");
+    return species_out(c, species, 1);
+}
+
+int dpd_get_species_ex(dpd_ctx *c, int64_t cap, int32_t *species, int32_t *ids, int64_t *n)
+{
+    if (!c) return DPD_ERR_ARG;
+    TRY(sync_check(c));
+    if (n) *n = c->n;
+    if (cap < c->n) return fail(c, DPD_ERR_ARG, "cap %lld < count %lld", (long long)cap, (long long)c->n);
+    TRY(species_out(c, species, 0));
     return copy_ids(c, ids);
 }
 

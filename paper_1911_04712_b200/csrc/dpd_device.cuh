@@ -26,6 +26,8 @@ struct Geom {
     int ncell;      // ext_x * ext_y * ext_z
 };
 
+constexpr int DPD_MAX_SPECIES = 4;
+
 // Pair-force parameters.
 struct PairP {
     float a;        // conservative amplitude
@@ -35,6 +37,11 @@ struct PairP {
     float rc2;      // r_c^2
     float power;    // k (w_R = w^k)                                         (C-4)
     uint32_t seed_fold; // seed lo ^ seed hi: key of the per-step key          (C-7)
+    // NEXT-2 species matrix (KMODE == 3 only): entry ti * DPD_MAX_SPECIES + tj holds the
+    // pair's a, gamma and sigma/sqrt(dt); ti, tj travel in vel.w
+    float sa[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
+    float sg[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
+    float ss[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
 };
 
 // Integrator parameters (C-2 item 3 / C-6).
@@ -102,16 +109,24 @@ __device__ __forceinline__ float weight_R(float w, float k)
 {
     if constexpr (KMODE == 0) return sqrt_approx(w);
     else if constexpr (KMODE == 1) return w;
-    else return w > 0.0f ? exp2f(k * __log2f(w)) : 0.0f;
+    else return w > 0.0f ? exp2f(k * __log2f(w)) : 0.0f; // 2 (generic k) and 3 (species matrix)
 }
 
 // Scalar pair force along d = r_i - r_j: returns s such that f_ij = s * d.
 //   mag = a w - gamma w_D (e . v_ij) + sigma/sqrt(dt) w_R xi ;  s = mag / r
-// r2 in (0, rc2) assumed.
+// r2 in (0, rc2) assumed.  KMODE 0: k = 1/2, 1: k = 1, 2: generic k, 3: generic k with the
+// species matrix (a, gamma, sigma of the pair looked up from the species in vel.w).
 template <int KMODE>
 __device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
-                                             uint32_t ks)
+                                             uint32_t ks, float vwi, float vwj)
 {
+    float a = pp.a, gamma = pp.gamma, sig_dt = pp.sig_dt;
+    if constexpr (KMODE == 3) {
+        const int t = __float_as_int(vwi) * DPD_MAX_SPECIES + __float_as_int(vwj);
+        a = pp.sa[t];
+        gamma = pp.sg[t];
+        sig_dt = pp.ss[t];
+    }
     const float rinv = rsqrtf(r2);
     const float r = r2 * rinv;
     const float w = fmaxf(__fmaf_rn(-r, pp.inv_rc, 1.0f), 0.0f);
@@ -119,7 +134,7 @@ __device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dv
     const float wD = (KMODE == 0) ? w : wR * wR;
     const uint2 wd = pair_words(idi, idj, ks);
     const float xi = box_muller(wd.x, wd.y);
-    const float mag = pp.a * w - pp.gamma * wD * (dvdot * rinv) + pp.sig_dt * wR * xi;
+    const float mag = a * w - gamma * wD * (dvdot * rinv) + sig_dt * wR * xi;
     return mag * rinv;
 }
 

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(128) k_force_halo(const float4 *__restrict__ p
                     if (r2 < pp.rc2 && r2 > 0.0f) {
                         const float4 vj = gvel[j];
                         const float dv = rx * (vi.x - vj.x) + ry * (vi.y - vj.y) + rz * (vi.z - vj.z);
-                        const float s = pair_scalar<KMODE>(pp, r2, dv, idi, (uint32_t)__float_as_int(pj.w), ks);
+                        const float s = pair_scalar<KMODE>(pp, r2, dv, idi, (uint32_t)__float_as_int(pj.w), ks, vi.w, vj.w);
                         Fx += s * rx;
                         Fy += s * ry;
                         Fz += s * rz;

@@ -214,7 +214,7 @@ __device__ __forceinline__ float pair_eval(const PairP &pp, const FixP &fx, floa
     const uint32_t idi = (uint32_t)__float_as_int(pi.w), idj = (uint32_t)__float_as_int(pj.w);
     float s = 0.0f;
     if (r2 > 0.0f) {
-        s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks);
+        s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks, vi.w, vj.w);
         if (fabsf(s) * (r2 * rsqrtf(r2)) > fx.mag_lim) raise_err(err, ERR_RANGE, (int)idi);
         if constexpr (RECORD) {
             const unsigned long long k = atomicAdd(rec.count, 1ull);
@@ -238,7 +238,7 @@ __device__ __forceinline__ float pair_core(const PairP &pp, float4 pi, float4 vi
     const float r2 = dx * dx + dy * dy + dz * dz;
     const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
     const float s = pair_scalar<KMODE>(pp, fmaxf(r2, 1e-30f), dvdot, (uint32_t)__float_as_int(pi.w),
-                                       (uint32_t)__float_as_int(pj.w), ks);
+                                       (uint32_t)__float_as_int(pj.w), ks, vi.w, vj.w);
     return r2 > 0.0f ? s : 0.0f;
 }
 

@@ -14,7 +14,7 @@
 namespace dpd {
 
 // Error word bits (device int err[4]: [0] flags, [1] offending id, [2] overflow amount)
-enum : int { ERR_NONFINITE = 1, ERR_CAPACITY = 2, ERR_RANGE = 4 };
+enum : int { ERR_NONFINITE = 1, ERR_CAPACITY = 2, ERR_RANGE = 4, ERR_SPECIES = 8 };
 
 __device__ __forceinline__ void raise_err(int *err, int bit, int id)
 {
@@ -111,9 +111,9 @@ __device__ __forceinline__ float4 *msg_data(const Msgs &m, int d)
 // rank's subdomain, in local coordinates.  *n_out counts the kept particles.
 // ---------------------------------------------------------------------------------------
 __global__ void k_pack_input(const float *__restrict__ pos3, const float *__restrict__ vel3,
-                             const int32_t *__restrict__ ids, int64_t n, Geom g, float3 gbox, float3 origin,
-                             float4 *__restrict__ pos4, float4 *__restrict__ vel4, float4 *__restrict__ frc4,
-                             int *n_out, int cap, int *err)
+                             const int32_t *__restrict__ ids, const int32_t *__restrict__ species, int nspecies,
+                             int64_t n, Geom g, float3 gbox, float3 origin, float4 *__restrict__ pos4,
+                             float4 *__restrict__ vel4, float4 *__restrict__ frc4, int *n_out, int cap, int *err)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool keep = false;
@@ -134,8 +134,13 @@ __global__ void k_pack_input(const float *__restrict__ pos3, const float *__rest
         y -= origin.y;
         z -= origin.z;
         keep = x >= 0.0f && x < g.L[0] && y >= 0.0f && y < g.L[1] && z >= 0.0f && z < g.L[2];
+        int sp = species ? species[i] : 0;
+        if (sp < 0 || sp >= nspecies) {
+            raise_err(err, ERR_SPECIES, id);
+            sp = 0;
+        }
         p4 = make_float4(x, y, z, __int_as_float(id));
-        v4 = make_float4(vx, vy, vz, 0.0f);
+        v4 = make_float4(vx, vy, vz, __int_as_float(sp)); // w: species index (NEXT-2)
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     const int lane = threadIdx.x & 31;
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(256) k_bin(const float4 *__restrict__ pos, con
                 if (slot < mig.cap[d]) {
                     float4 *q = msg_data(mig, d) + 2 * slot;
                     q[0] = make_float4(xn.x, xn.y, xn.z, p.w);
-                    q[1] = make_float4(un.x, un.y, un.z, 0.0f);
+                    q[1] = make_float4(un.x, un.y, un.z, v.w); // w: species
                 } else {
                     raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
                 }
@@ -382,7 +387,7 @@ __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos,
     const int c = cell_index(g, xn.x, xn.y, xn.z);
     const int dst = start[c] + rank[i];
     pos_o[dst] = make_float4(xn.x, xn.y, xn.z, p.w);
-    vel_o[dst] = make_float4(un.x, un.y, un.z, 0.0f);
+    vel_o[dst] = make_float4(un.x, un.y, un.z, v.w); // w: species
     frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 }
 
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ po
                 const float4 vj = vel[j];
                 const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
                 const uint32_t idj = (uint32_t)__float_as_int(pj.w);
-                const float s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks);
+                const float s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks, vi.w, vj.w);
                 Fx += s * dx;
                 Fy += s * dy;
                 Fz += s * dz;
@@ -498,6 +503,15 @@ __global__ void k_ids_cells(const float4 *__restrict__ pos, int n, Geom g, int32
     const int id = __float_as_int(p.w);
     if (ids) ids[i] = id;
     if (cell_of_id) cell_of_id[id] = cell_index(g, p.x, p.y, p.z);
+}
+
+// Species index (vel.w, NEXT-2) per particle, in id order (by_id) or storage order.
+__global__ void k_species_out(const float4 *__restrict__ pos, const float4 *__restrict__ vel, int n,
+                              int32_t *__restrict__ out, int by_id)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[by_id ? __float_as_int(pos[i].w) : i] = __float_as_int(vel[i].w);
 }
 
 // Raw-state copy in storage order (x in global coordinates, u, F as float3 rows).
