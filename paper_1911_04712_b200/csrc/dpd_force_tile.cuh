@@ -31,10 +31,10 @@ constexpr int FT_NSC = FT_SX * FT_SY * FT_SZ; // staged cells (108)
 constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
 constexpr int FT_NTHR = 288;                  // 9 warps: ~28 home particles each (balanced ranges)
 constexpr int FT_NWARP = FT_NTHR / 32;
-constexpr int FT_SCAP = 1152;                 // staged particles (mean 864, sd 29 at rho = 8)
+constexpr int FT_SCAP = 1024;                 // staged particles (mean 864, sd 29 at rho = 8: 5.5 sd)
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
-constexpr int FT_LCAP = 48;                   // hits per home particle (mean 16.8)
-constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 25 words per list (odd): conflict-free appends
+constexpr int FT_LCAP = 40;                   // hits per home particle (mean 16.8, sd 4.1)
+constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 21 words per list (odd): conflict-free appends
 constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32 owners + sentinel)
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
@@ -46,11 +46,12 @@ struct FixP {
 };
 
 struct ForceTileSmem {
-    float4 sp[FT_SCAP];                          // staged positions (tile frame), w = id bits
-    float4 sv[FT_SCAP];                          // staged velocities
-    float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // SoA copy of the positions for the sweep
+    float4 sv[FT_SCAP];                       // staged velocities (w: species)
+    unsigned short lst[FT_NTHR * FT_LSTRIDE]; // per-thread pair lists (one home particle each);
+                                              // during staging: the AoS landing buffer of the positions
+    float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // staged positions (tile frame), SoA
+    int sid[FT_SCAP];                            // staged ids
     int acc[3][FT_SCAP];                         // fixed-point force sums
-    unsigned short lst[FT_NTHR * FT_LSTRIDE];    // per-thread pair lists (one home particle each)
     int woex[FT_NWARP * FT_WSTRIDE];             // per warp: compacted owners' list prefix (+ total)
     int wsi[FT_NWARP * FT_WSTRIDE];              //   staged index of the owner
     int wrow[FT_NWARP * FT_WSTRIDE];             //   list base minus prefix
@@ -70,6 +71,18 @@ __device__ __forceinline__ int ext_coord(int c, int n, int split)
 {
     if (split) return c + 1;
     return c < 0 ? c + n : (c >= n ? c - n : c);
+}
+
+static_assert(sizeof(unsigned short) * FT_NTHR * FT_LSTRIDE >= sizeof(float4) * FT_SCAP,
+              "the list area doubles as the position landing buffer");
+static_assert(offsetof(ForceTileSmem, lst) % 16 == 0 && offsetof(ForceTileSmem, sx) % 8 == 0 &&
+                  offsetof(ForceTileSmem, sy) % 8 == 0 && offsetof(ForceTileSmem, sz) % 8 == 0,
+              "cp.async / packed-pair alignment");
+
+// Staged position j as (x, y, z, id bits).
+__device__ __forceinline__ float4 ldp(const ForceTileSmem &S, int j)
+{
+    return make_float4(S.sx[j], S.sy[j], S.sz[j], __int_as_float(S.sid[j]));
 }
 
 __device__ __forceinline__ int to_fixed(float f, float scale)
@@ -167,7 +180,7 @@ __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__res
                                            const float4 *__restrict__ vel, int g0, int s0, int len, int lane)
 {
     for (int k = lane; k < len; k += 32) {
-        cp_async16(&S.sp[s0 + k], &pos[g0 + k]);
+        cp_async16(reinterpret_cast<float4 *>(S.lst) + s0 + k, &pos[g0 + k]);
         cp_async16(&S.sv[s0 + k], &vel[g0 + k]);
     }
 }
@@ -177,12 +190,11 @@ __device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, flo
 {
     for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
-        const float4 p = S.sp[s];
-        const float px = p.x + sx, py = p.y + sy, pz = p.z + sz;
-        S.sp[s] = make_float4(px, py, pz, p.w);
-        S.sx[s] = px;
-        S.sy[s] = py;
-        S.sz[s] = pz;
+        const float4 p = reinterpret_cast<const float4 *>(S.lst)[s];
+        S.sx[s] = p.x + sx;
+        S.sy[s] = p.y + sy;
+        S.sz[s] = p.z + sz;
+        S.sid[s] = __float_as_int(p.w);
         S.acc[0][s] = 0;
         S.acc[1][s] = 0;
         S.acc[2][s] = 0;
@@ -284,7 +296,7 @@ __device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &
     c.enext = S.woex[c.o + 1];
     c.si = S.wsi[c.o];
     c.lrow = S.wrow[c.o];
-    c.pi = S.sp[c.si];
+    c.pi = ldp(S, c.si);
     c.vi = S.sv[c.si];
 }
 
@@ -307,7 +319,7 @@ __device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
         c.enext = S.woex[c.o + 1];
         c.si = S.wsi[c.o];
         c.lrow = S.wrow[c.o];
-        c.pi = S.sp[c.si];
+        c.pi = ldp(S, c.si);
         c.vi = S.sv[c.si];
     }
     return S.lst[c.lrow + c.t];
@@ -385,7 +397,7 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
 }
 
 template <bool RECORD, int KMODE>
-__global__ void __launch_bounds__(FT_NTHR, 2)
+__global__ void __launch_bounds__(FT_NTHR, 3)
     k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
                  const int *__restrict__ start, Geom g, PairP pp, FixP fx, uint32_t s_lo, uint32_t s_hi,
                  PairRec rec, int *err)
@@ -569,12 +581,12 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
                     a = e;
                 }
                 if (full) {
-                    const float4 pi = S.sp[s_i], vi = S.sv[s_i];
+                    const float4 pi = ldp(S, s_i), vi = S.sv[s_i];
                     for (; a < b; ++a) {
                         if (!(r2_one(S, a, px, py, pz) < pp.rc2)) continue;
                         float dx, dy, dz;
                         const float s =
-                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, S.sp[a], S.sv[a], ks, rec, err, dx, dy, dz);
+                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp(S, a), S.sv[a], ks, rec, err, dx, dy, dz);
                         const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
                                   qz = to_fixed(s * dz, fx.scale);
                         atomicAdd(&S.acc[0][s_i], qx);
@@ -620,10 +632,10 @@ __global__ void __launch_bounds__(FT_NTHR, 2)
                 const bool bact = B.t < B.t1;
                 const int jb = bact ? cursor_next(B, S) : B.si; // inactive: self pair, r2 = 0 -> f = 0
                 float dxa, dya, dza, dxb, dyb, dzb;
-                const float sa = pair_core<KMODE>(pp, A.pi, A.vi, S.sp[ja], S.sv[ja], ks, dxa, dya, dza);
-                const float sb = pair_core<KMODE>(pp, B.pi, B.vi, S.sp[jb], S.sv[jb], ks, dxb, dyb, dzb);
-                pair_checks<RECORD>(pp, fx, A.pi, S.sp[ja], sa, dxa, dya, dza, ks, rec, err);
-                if (bact) pair_checks<RECORD>(pp, fx, B.pi, S.sp[jb], sb, dxb, dyb, dzb, ks, rec, err);
+                const float sa = pair_core<KMODE>(pp, A.pi, A.vi, ldp(S, ja), S.sv[ja], ks, dxa, dya, dza);
+                const float sb = pair_core<KMODE>(pp, B.pi, B.vi, ldp(S, jb), S.sv[jb], ks, dxb, dyb, dzb);
+                pair_checks<RECORD>(pp, fx, A.pi, ldp(S, ja), sa, dxa, dya, dza, ks, rec, err);
+                if (bact) pair_checks<RECORD>(pp, fx, B.pi, ldp(S, jb), sb, dxb, dyb, dzb, ks, rec, err);
                 cursor_accumulate(A, S, ja, sa, dxa, dya, dza, fx.scale);
                 if (bact) cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale);
             }
