@@ -283,3 +283,63 @@ def test_full_size_sampled_parity(name, kernel):
     _, ocount, ostart = oracle.cells(p, by_id(ids, pos)[0])
     assert np.array_equal(count, ocount) and np.array_equal(start, ostart)
     assert np.abs(F.astype(np.float64).sum(0)).max() < 1e-5 * np.abs(F).sum()
+
+
+# Boxes whose cell grids leave ragged tiles in every dimension (the tile is 4 x 4 x 2 home
+# cells), non-integer cell edges (h = L / floor(L) > r_c), the 3-cell minimum where
+# the stencil wraps onto itself, and strongly anisotropic shapes.
+RAGGED_BOXES = [(11.3, 9.7, 7.2), (3.0, 3.0, 3.0), (3.5, 17.0, 5.0), (13.0, 4.0, 9.0), (6.0, 5.0, 3.2)]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("box", RAGGED_BOXES)
+@pytest.mark.parametrize("rho", [3.0, 8.0])
+def test_per_step_parity_ragged_boxes(box, rho, kernel):
+    """10 steps (C-13 protocol) on ragged / minimal / anisotropic boxes: cells bit-exact,
+    forces within the bar, every particle accounted for."""
+    cfg = workloads.Config("ragged", box, rho, 25.0, 4.5, 1.0, 0.5, 0.01)
+    p = _params(cfg)
+    eps = boundary_eps(cfg.box)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg, kernel=kernel)
+    d.set_particles(pos0, vel0)
+    n = pos0.shape[0]
+    for s in range(11):
+        pos, u, F, ids = d.get_state()
+        assert np.array_equal(np.sort(ids), np.arange(n))
+        x_id, u_id, F_id = by_id(ids, pos, u, F)
+        cell, count, start = d.debug_cells()
+        ocell, ocount, ostart = oracle.cells(p, x_id)
+        assert np.array_equal(count, ocount) and np.array_equal(start, ostart) and np.array_equal(cell, ocell)
+        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps)
+        check_forces(F_id, F_ref, allow)
+        if s < 10:
+            d.step(1)
+
+
+@pytest.mark.parametrize("name", ["pois96", "weak128"])
+def test_full_size_sampled_parity_other_configs(name):
+    """BASELINE configs 3 and 4 at full size (7.1 M / 16.8 M particles) in bench's launch
+    configuration: sampled all-j sums against the oracle, cell counts bit-exact, sum F = 0."""
+    cfg = workloads.CONFIGS[name]
+    p = _params(cfg)
+    eps = boundary_eps(cfg.box)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    if cfg.body_f:
+        d.set_body_force(cfg.body_f)
+    d.set_particles(pos0, vel0)
+    d.step(3)
+    pos, u, F, ids = d.get_state()
+    n = pos.shape[0]
+    assert n == pos0.shape[0]
+    rng = np.random.default_rng(1)
+    sel = rng.choice(n, 32, replace=False)
+    F_ref, allow = oracle.forces_subset(p, pos, u, d.get_step(), sel, ids=ids.astype(np.uint32), eps=eps)
+    scale = np.abs(F).max()
+    err = np.abs(F[sel].astype(np.float64) - F_ref).max(axis=1)
+    assert np.all(err <= FORCE_TOL * scale + allow), (err.max(), scale)
+    _, count, start = d.debug_cells()
+    _, ocount, ostart = oracle.cells(p, by_id(ids, pos)[0])
+    assert np.array_equal(count, ocount) and np.array_equal(start, ostart)
+    assert np.abs(F.astype(np.float64).sum(0)).max() < 1e-5 * np.abs(F).sum()
