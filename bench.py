@@ -86,6 +86,17 @@ def kernel_roofline(name, ms_per_launch, cfg, n_local, peaks, src):
             "frac": ach / float(peaks["hbm_gbs"]), "traffic": None, "peak_source": src}
 
 
+def kernel_traffic():
+    """DRAM bytes per launch from the committed `ncu --set full` capture (tools/ncu_traffic.py);
+    None when absent."""
+    path = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    if not os.path.exists(path):
+        return {}, None
+    with open(path) as fh:
+        d = json.load(fh)
+    return d.get("per_launch", {}), "profiles/kernel_traffic.json (" + d.get("source", "?") + ")"
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -222,6 +233,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-kernel", type=int, default=None, help="0 tiled, 1 reference, 2 cell-warp")
+    ap.add_argument("--option", action="append", default=[], help="engine option name=value (dpd_set_option)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = workloads.CONFIGS[args.config]
@@ -261,6 +273,9 @@ def main():
     capi.dpd_set_stream(ctx, stream.cuda_stream)
     if args.force_kernel is not None:
         capi.dpd_set_option(ctx, "force_kernel", args.force_kernel)
+    for opt in args.option:
+        name, val = opt.split("=")
+        capi.dpd_set_option(ctx, name, int(val))
     if cfg.body_f:
         capi.dpd_set_body_force(ctx, cfg.body_f)
     # each rank generates only its own subdomain's particles with globally unique ids
@@ -350,6 +365,13 @@ def main():
     roof = None
     if dom:
         roof = kernel_roofline(dom, per_kernel[dom]["ms_per_launch"], cfg, n_local, peaks, peaks_src)
+        traffic, tsrc = kernel_traffic()
+        t = traffic.get(dom)
+        if t and t.get("workload") == cfg.name and int(t.get("n_local", -1)) == int(n_local):
+            roof["traffic"] = t["dram_bytes"]
+            roof["traffic_source"] = tsrc
+            roof["traffic_vs_algorithmic"] = t["dram_bytes"] / (48.0 * n_local) if dom == "force" else \
+                t["dram_bytes"] / max(1.0, KERNEL_BYTES.get(dom, 0.0) * n_local)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

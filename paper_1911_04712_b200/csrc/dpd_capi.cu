@@ -769,6 +769,7 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     pp.seed_fold = (uint32_t)seed ^ (uint32_t)(seed >> 32);
     c->pp = pp;
     set_fixed_scale(c, a, gamma);
+    c->fix.prune = 1;
     {
         // two tiles per SM need the maximum shared-memory carveout (2 x (smem + 1 KB) <= 228 KB)
         const int smem = (int)sizeof(ForceTileSmem);
@@ -976,6 +977,11 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
             return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled), 1 (reference) or 2 (cell-warp)");
         if (value != 0 && c->dist) return fail(c, DPD_ERR_ARG, "force_kernel %d is single-domain only", (int)value);
         c->force_impl = (int)value;
+        return DPD_OK;
+    }
+    if (strcmp(name, "row_pruning") == 0) {
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "row_pruning must be 0 or 1");
+        c->fix.prune = (int)value;
         return DPD_OK;
     }
     if (strcmp(name, "message_capacity_percent") == 0) {

@@ -43,6 +43,7 @@ struct FixP {
     float inv_scale; // 2^-k
     float mag_lim;   // 2^21 / scale: larger pair magnitudes raise ERR_RANGE
     float slack;     // row-end pruning: distance bounds are lowered by this much
+    int prune;       // row-end pruning on (1, default) / off (0): engine option "row_pruning"
 };
 
 struct ForceTileSmem {
@@ -559,7 +560,7 @@ __global__ void __launch_bounds__(FT_NTHR, 3)
                 const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
                 int a = (k == 0) ? s_i + 1 : S.soff[cs];
                 int b = S.soff[cs + (k == 0 ? 2 : 3)];
-                if (k > 0) {
+                if (k > 0 && fx.prune) {
                     const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
                     const float qz = (k == 1) ? 0.0f : dzr;
                     const float q = qy * qy + qz * qz;
