@@ -37,7 +37,9 @@ class Params(C.Structure):
                 ("gamma", C.c_double), ("kT", C.c_double), ("power", C.c_double),
                 ("dt", C.c_double), ("seed", C.c_uint64), ("body_f", C.c_double),
                 ("nspecies", C.c_int32), ("amat", C.c_double * 16), ("gmat", C.c_double * 16),
-                ("species", C.POINTER(C.c_int32))]
+                ("species", C.POINTER(C.c_int32)),
+                ("nwall", C.c_int32), ("wtype", C.c_int32 * 4), ("wprm", C.c_double * 16),
+                ("wvel", C.c_double * 12), ("frozen_mask", C.c_int32), ("body_mode", C.c_int32)]
 
 
 @dataclass
@@ -56,6 +58,11 @@ class DPDParams:
     amat: object = None
     gmat: object = None
     species: object = None
+    # NEXT-3 walls: list of (type, (p0, p1, p2, p3), (uwx, uwy, uwz)); type 1 plane
+    # s = n.x - c with (n, c); 2/3/4 cylinder along x/y/z with (c1, c2, R, sign)
+    walls: object = None
+    frozen_mask: int = 0
+    body_mode: int = 0  # 0 periodic Poiseuille, 1 uniform +f along z
 
     def c(self) -> Params:
         p = Params()
@@ -74,9 +81,21 @@ class DPDParams:
                 p.amat[k] = float(val)
             for k, val in enumerate(G.ravel()):
                 p.gmat[k] = float(val)
-            if self.species is not None:
-                self._sp = np.ascontiguousarray(self.species, np.int32)  # kept alive with p
-                p.species = self._sp.ctypes.data_as(C.POINTER(C.c_int32))
+        if self.species is not None:
+            self._sp = np.ascontiguousarray(self.species, np.int32)  # kept alive with p
+            p.species = self._sp.ctypes.data_as(C.POINTER(C.c_int32))
+        if self.walls:
+            if len(self.walls) > 4:
+                raise ValueError("at most 4 wall primitives")
+            p.nwall = len(self.walls)
+            for k, (t, prm, uw) in enumerate(self.walls):
+                p.wtype[k] = int(t)
+                for c in range(4):
+                    p.wprm[4 * k + c] = float(prm[c])
+                for c in range(3):
+                    p.wvel[3 * k + c] = float(uw[c])
+        p.frozen_mask = int(self.frozen_mask)
+        p.body_mode = int(self.body_mode)
         return p
 
 
@@ -116,6 +135,12 @@ def lib():
         L.oracle_step_celllist.argtypes = [P(Params), i64, dp, dp, dp, P(u32), P(i64), i64]
         L.oracle_step_celllist.restype = C.c_int
         L.oracle_num_threads.restype = C.c_int
+        L.oracle_wall_sdf.argtypes = [P(Params), dp, dp]
+        L.oracle_wall_sdf.restype = d
+        L.oracle_kick_drift.argtypes = [P(Params), i64, dp, dp, dp, d]
+        L.oracle_kick_drift.restype = i64
+        L.oracle_wall_carve.argtypes = [P(Params), i64, dp, dp, P(C.c_int32), C.c_int32, P(C.c_uint8)]
+        L.oracle_wall_carve.restype = i64
         _lib = L
     return _lib
 
@@ -323,3 +348,35 @@ class State:
                               _p(self.u, C.c_double))
         self.s = int(s.value)
         return self
+
+
+def wall_sdf(p: DPDParams, x):
+    """s(x) = max over the wall primitives (C-23) and the wall velocity there, per row."""
+    x = _f64(np.atleast_2d(x))
+    pc = p.c()
+    s = np.empty(len(x))
+    uw = np.empty((len(x), 3))
+    for i in range(len(x)):
+        row = np.ascontiguousarray(x[i])
+        s[i] = lib().oracle_wall_sdf(C.byref(pc), _p(row, C.c_double), _p(uw[i], C.c_double))
+    return s, uw
+
+
+def kick_drift(p: DPDParams, x, v, F, kick: float):
+    """One kick-drift with bounce-back (C-6, C-23); returns (x', u', bounces)."""
+    x, v, F = _f64(x).copy(), _f64(v).copy(), _f64(F)
+    pc = p.c()
+    nb = lib().oracle_kick_drift(C.byref(pc), x.shape[0], _p(x, C.c_double), _p(v, C.c_double),
+                                 _p(F, C.c_double), float(kick))
+    return x, v, int(nb)
+
+
+def wall_carve(p: DPDParams, x, v, species, wall_species: int):
+    """Frozen layer (C-23): returns (keep mask, v', species', n_frozen)."""
+    x, v = _f64(x), _f64(v).copy()
+    sp = np.ascontiguousarray(species, np.int32).copy()
+    keep = np.zeros(x.shape[0], np.uint8)
+    pc = p.c()
+    nf = lib().oracle_wall_carve(C.byref(pc), x.shape[0], _p(x, C.c_double), _p(v, C.c_double),
+                                 _p(sp, C.c_int32), int(wall_species), _p(keep, C.c_uint8))
+    return keep.astype(bool), v, sp, int(nf)

@@ -20,6 +20,7 @@
  *   - observables: kinetic T (full-step v), conservative virial p       (C-14, C-15)
  *   - an fp64 cell-list sweep (CPU timing mode, never used as truth)    (C-2 item 7)
  *   - per-pair (a, gamma) from a species matrix
+ *   - SDF walls: frozen layer, bounce-back
  *
  * Parity pins: see tests/test_oracle_*.py (Random123 KATs, hand examples S:194/S:196,
  * closed forms, invariants, brute force vs cell list, T = kT, Groot-Warren EOS).
@@ -50,7 +51,50 @@ typedef struct {
     double amat[16];         /* nspecies x nspecies, row-major (nspecies <= 4)        */
     double gmat[16];
     const int32_t *species;  /* species of particle index i (NULL: all 0)             */
+    /* SDF walls, reading C-23: the solid is the
+     * union of up to 4 primitives, s(x) = max_k s_k(x) > 0 inside the solid; particles of
+     * a frozen species (bit s of frozen_mask) never move and keep the wall velocity.     */
+    int32_t nwall;           /* number of primitives (0: no walls)                     */
+    int32_t wtype[4];        /* 1 plane: s = n.x - c, prm (nx, ny, nz, c), |n| = 1;
+                                2/3/4 cylinder along x/y/z: prm (c1, c2, R, sign),
+                                s = sign (R - dist to the axis) (+1 post, -1 pipe)     */
+    double wprm[16];
+    double wvel[12];         /* translational wall velocity of each primitive           */
+    int32_t frozen_mask;
+    int32_t body_mode;       /* 0: periodic Poiseuille; 1: uniform +f along z */
 } oracle_params;
+
+/* Signed distance of one primitive (C-23). */
+static double wall_prim(const oracle_params *p, int k, const double x[3])
+{
+    const double *q = &p->wprm[4 * k];
+    if (p->wtype[k] == 1) return q[0] * x[0] + q[1] * x[1] + q[2] * x[2] - q[3];
+    const int ax = p->wtype[k] - 2, a = (ax + 1) % 3, b = (ax + 2) % 3;
+    const double da = x[a] - q[0], db = x[b] - q[1];
+    return q[3] * (q[2] - sqrt(da * da + db * db));
+}
+
+/* s(x) = max_k s_k(x) (union of solids); uw (may be NULL) = velocity of the maximising
+ * primitive.  Without walls s = -inf. */
+double oracle_wall_sdf(const oracle_params *p, const double x[3], double uw[3])
+{
+    double best = -INFINITY;
+    int arg = -1;
+    for (int k = 0; k < p->nwall; ++k) {
+        double sk = wall_prim(p, k, x);
+        if (sk > best) { best = sk; arg = k; }
+    }
+    if (uw) {
+        for (int c = 0; c < 3; ++c) uw[c] = arg >= 0 ? p->wvel[3 * arg + c] : 0.0;
+    }
+    return best;
+}
+
+static int is_frozen(const oracle_params *p, int64_t i)
+{
+    const int32_t sp = p->species ? p->species[i] : 0;
+    return (p->frozen_mask >> sp) & 1;
+}
 
 /* The parameters of pair (i, j): p itself, or a copy with the pair's (a, gamma). */
 static const oracle_params *pair_params(const oracle_params *p, int64_t i, int64_t j, oracle_params *q)
@@ -371,10 +415,79 @@ static double wrap1(double x, double L)
     return x;
 }
 
-/* Periodic-Poiseuille body force: (0,0,-f) for r_x <= L/2, else (0,0,+f). */
+/* Body force along z: periodic Poiseuille: (0,0,-f) for r_x <= L/2, else
+ * (0,0,+f); body_mode 1: uniform (0,0,+f) (wall-bounded Poiseuille, NEXT-3). */
 static double body_fz(const oracle_params *p, double rx)
 {
+    if (p->body_mode == 1) return p->body_f;
     return rx <= 0.5 * p->box[0] ? -p->body_f : p->body_f;
+}
+
+/* Kick-drift of one particle with wall bounce-back (C-6, C-23): u = v + kick
+ * (F + f_body); x' = x + dt u.  If x' is inside the solid (s > 0) the collision time
+ * t* in [0, dt] with s(x + t u) = 0 is found by bisection (80 halvings in fp64), the
+ * particle is placed at x + t_lo u (the last point with s <= 0) and its velocity is
+ * reversed in the wall frame, u <- 2 u_w - u.  Frozen particles do not move.  x' is then
+ * wrapped (C-10).  Returns 1 if the particle bounced. */
+static int kick_drift_one(const oracle_params *p, int64_t i, double *x, double *v, const double *F,
+                          double kick)
+{
+    if (is_frozen(p, i)) return 0;
+    double fz = body_fz(p, x[0]);
+    double u[3] = {v[0] + kick * F[0], v[1] + kick * F[1], v[2] + kick * (F[2] + fz)};
+    double xn[3] = {x[0] + p->dt * u[0], x[1] + p->dt * u[1], x[2] + p->dt * u[2]};
+    int bounced = 0;
+    if (p->nwall > 0 && oracle_wall_sdf(p, xn, NULL) > 0.0) {
+        double lo = 0.0, hi = p->dt;
+        if (oracle_wall_sdf(p, x, NULL) > 0.0) {
+            hi = 0.0; /* already inside (never for a valid state): stay, reverse */
+        } else {
+            for (int it = 0; it < 80; ++it) {
+                double mid = 0.5 * (lo + hi), xm[3];
+                for (int c = 0; c < 3; ++c) xm[c] = x[c] + mid * u[c];
+                if (oracle_wall_sdf(p, xm, NULL) > 0.0) hi = mid; else lo = mid;
+            }
+        }
+        double uw[3];
+        for (int c = 0; c < 3; ++c) xn[c] = x[c] + lo * u[c];
+        oracle_wall_sdf(p, xn, uw);
+        for (int c = 0; c < 3; ++c) u[c] = 2.0 * uw[c] - u[c];
+        bounced = 1;
+    }
+    for (int c = 0; c < 3; ++c) {
+        x[c] = wrap1(xn[c], p->box[c]);
+        v[c] = u[c];
+    }
+    return bounced;
+}
+
+/* One kick-drift (+ bounce-back) of every particle in place: v <- u, x <- x'.  Returns the
+ * number of bounces.  The per-step parity test predicts the GPU's x_s, u_s with it. */
+int64_t oracle_kick_drift(const oracle_params *p, int64_t n, double *x, double *v, const double *F, double kick)
+{
+    int64_t nb = 0;
+    for (int64_t i = 0; i < n; ++i) nb += kick_drift_one(p, i, &x[3 * i], &v[3 * i], &F[3 * i], kick);
+    return nb;
+}
+
+/* Carve a fluid configuration with the walls (C-23): particles with s > r_c are
+ * removed (keep[i] = 0), those with 0 < s <= r_c become the frozen layer (species :=
+ * wall_species, v := u_w(x)), the rest is untouched.  Returns the number of frozen. */
+int64_t oracle_wall_carve(const oracle_params *p, int64_t n, const double *x, double *v, int32_t *species,
+                          int32_t wall_species, uint8_t *keep)
+{
+    int64_t nf = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double uw[3];
+        double sd = oracle_wall_sdf(p, &x[3 * i], uw);
+        keep[i] = sd <= p->rc;
+        if (sd > 0.0 && sd <= p->rc) {
+            species[i] = wall_species;
+            for (int c = 0; c < 3; ++c) v[3 * i + c] = uw[c];
+            ++nf;
+        }
+    }
+    return nf;
 }
 
 /* Prime (C-2 item 2): F = PairForces(x, v, s). */
@@ -398,17 +511,15 @@ int oracle_step(const oracle_params *p, int64_t n, double *x, double *v, double 
     double *u = (double *)malloc(sizeof(double) * 3 * (size_t)(n > 0 ? n : 1));
     if (!u) return 1;
     for (int64_t it = 0; it < nsteps; ++it) {
-        for (int64_t i = 0; i < n; ++i) {
-            double fz = body_fz(p, x[3 * i + 0]);
-            u[3 * i + 0] = v[3 * i + 0] + 0.5 * p->dt * F[3 * i + 0];
-            u[3 * i + 1] = v[3 * i + 1] + 0.5 * p->dt * F[3 * i + 1];
-            u[3 * i + 2] = v[3 * i + 2] + 0.5 * p->dt * (F[3 * i + 2] + fz);
-            for (int k = 0; k < 3; ++k)
-                x[3 * i + k] = wrap1(x[3 * i + k] + p->dt * u[3 * i + k], p->box[k]);
-        }
+        memcpy(u, v, sizeof(double) * 3 * (size_t)n);
+        oracle_kick_drift(p, n, x, u, F, 0.5 * p->dt);
         *step += 1;
         oracle_forces(p, n, x, u, ids, *step, 0.0, F, NULL, NULL);
         for (int64_t i = 0; i < n; ++i) {
+            if (is_frozen(p, i)) { /* the wall velocity, unchanged */
+                for (int k = 0; k < 3; ++k) v[3 * i + k] = u[3 * i + k];
+                continue;
+            }
             double fz = body_fz(p, x[3 * i + 0]);
             v[3 * i + 0] = u[3 * i + 0] + 0.5 * p->dt * F[3 * i + 0];
             v[3 * i + 1] = u[3 * i + 1] + 0.5 * p->dt * F[3 * i + 1];
@@ -536,17 +647,15 @@ int oracle_step_celllist(const oracle_params *p, int64_t n, double *x, double *v
     if (!u) return 1;
     int rc = 0;
     for (int64_t it = 0; it < nsteps && rc == 0; ++it) {
-        for (int64_t i = 0; i < n; ++i) {
-            double fz = body_fz(p, x[3 * i + 0]);
-            u[3 * i + 0] = v[3 * i + 0] + 0.5 * p->dt * F[3 * i + 0];
-            u[3 * i + 1] = v[3 * i + 1] + 0.5 * p->dt * F[3 * i + 1];
-            u[3 * i + 2] = v[3 * i + 2] + 0.5 * p->dt * (F[3 * i + 2] + fz);
-            for (int k = 0; k < 3; ++k)
-                x[3 * i + k] = wrap1(x[3 * i + k] + p->dt * u[3 * i + k], p->box[k]);
-        }
+        memcpy(u, v, sizeof(double) * 3 * (size_t)n);
+        oracle_kick_drift(p, n, x, u, F, 0.5 * p->dt);
         *step += 1;
         rc = oracle_forces_celllist(p, n, x, u, ids, *step, F, NULL);
         for (int64_t i = 0; i < n; ++i) {
+            if (is_frozen(p, i)) {
+                for (int k = 0; k < 3; ++k) v[3 * i + k] = u[3 * i + k];
+                continue;
+            }
             double fz = body_fz(p, x[3 * i + 0]);
             v[3 * i + 0] = u[3 * i + 0] + 0.5 * p->dt * F[3 * i + 0];
             v[3 * i + 1] = u[3 * i + 1] + 0.5 * p->dt * F[3 * i + 1];
