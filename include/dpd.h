@@ -79,6 +79,8 @@ int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
  *                  to fp32 summation order).  1 and 2 are single-domain only.
  *   "message_capacity_percent" (distributed contexts) scales the per-direction message
  *                  capacities (default 100; >= 10).
+ *   "body_force_mode" 0 = periodic Poiseuille (default), 1 = uniform +f along z.
+ *   "row_pruning"  1 = prune stencil rows / end cells farther than r_c (default), 0 = off.
  * Out-of-range values -> DPD_ERR_ARG; unknown names -> DPD_ERR_ARG. */
 int dpd_set_option(dpd_ctx *ctx, const char *name, int64_t value);
 
@@ -103,9 +105,44 @@ int dpd_get_stat(dpd_ctx *ctx, const char *name, int64_t *value);
  * non-finite or asymmetric entries). */
 int dpd_set_species(dpd_ctx *ctx, int nspecies, const double *a, const double *gamma);
 
+/* SDF walls (reading C-23).  The solid is the
+ * union of nprim <= 4 primitives, s(x) = max_k s_k(x) > 0 inside the solid, in GLOBAL
+ * coordinates:
+ *   type 1 plane:      prm = (nx, ny, nz, c), |n| = 1, s = n.x - c
+ *   type 2/3/4 cylinder along x/y/z: prm = (c1, c2, R, sign) with (c1, c2) the axis in the
+ *                      two other coordinates (cyclic order), s = sign (R - distance to the
+ *                      axis): sign +1 a solid post, -1 a pipe (solid outside)
+ *   uw[3k..3k+2]       translational velocity of primitive k (moving walls, Couette)
+ * Every step, a fluid particle whose drift ends inside the solid is put back at its
+ * collision point (bisection on t in [0, dt]) and its velocity is reversed in the wall
+ * frame, u <- 2 u_w - u, where u_w is that of the primitive with the largest s there.
+ * nprim = 0 removes the walls.  Errors: DPD_ERR_ARG (nprim > 4, NULL arrays),
+ * DPD_ERR_CONFIG (unknown type, non-unit normal, R <= 0, sign not +-1, non-finite). */
+int dpd_set_walls(dpd_ctx *ctx, int nprim, const int32_t *type, const double *prm, const double *uw);
+
+/* Species whose particles never move (bit s of mask set): the frozen wall layer.  Their
+ * velocity stays the wall velocity; they still interact with the fluid. */
+int dpd_set_frozen_species(dpd_ctx *ctx, int32_t mask);
+
+/* Carve the current configuration with the walls: particles with s > r_c are
+ * removed, those with 0 < s <= r_c become frozen particles of species wall_species with
+ * the wall velocity (wall_species is added to the frozen mask), fluid velocities are
+ * completed to full-step values, the survivors are re-sorted and the forces re-primed at
+ * the current step.  On one domain with dense ids the ids are renumbered densely (kept
+ * particles keep their id order).  *n_frozen / *n_removed (may be NULL) receive this
+ * rank's counts.  Collective in distributed contexts; group members must have been primed.
+ * wall_species < nspecies when a species matrix is set, else <= 30. */
+int dpd_wall_carve(dpd_ctx *ctx, int32_t wall_species, int64_t *n_frozen, int64_t *n_removed);
+
+/* Device SDF s(x) of the current walls at n global points x (n x 3 float32) -> sdf[n]
+ * (test hook; -3e38 without walls). */
+int dpd_wall_sdf(dpd_ctx *ctx, int64_t n, const float *x, float *sdf);
+
 /* Periodic-Poiseuille body force: f_body = (0,0,-f) for r_x <= L_x/2 and
- * (0,0,+f) otherwise (global coordinates).  f = 0 (default) disables it.  The body force
- * enters the integrator, not dpd_get_forces. */
+ * (0,0,+f) otherwise (global coordinates); with the engine option "body_force_mode" = 1
+ * it is the uniform (0,0,+f) of a wall-bounded channel.  f = 0 (default) disables it.
+ * The body force acts on non-frozen particles and enters the integrator, not
+ * dpd_get_forces. */
 int dpd_set_body_force(dpd_ctx *ctx, double f);
 
 /* Load n particles (copied; the caller keeps its buffers), assign ids 0..n-1, set the

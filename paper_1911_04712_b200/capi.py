@@ -68,6 +68,10 @@ SIGNATURES = [
     ("dpd_get_particles_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _P(C.c_int64)]),
     ("dpd_get_forces_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _P(C.c_int64)]),
     ("dpd_get_species", C.c_int, [_vp, C.c_int64, _vp]),
+    ("dpd_set_walls", C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
+    ("dpd_set_frozen_species", C.c_int, [_vp, C.c_int32]),
+    ("dpd_wall_carve", C.c_int, [_vp, C.c_int32, _P(C.c_int64), _P(C.c_int64)]),
+    ("dpd_wall_sdf", C.c_int, [_vp, C.c_int64, _vp, _vp]),
     ("dpd_get_species_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _P(C.c_int64)]),
     ("dpd_debug_philox", C.c_int, [C.c_int64, _vp, _vp, _vp]),
     ("dpd_debug_pair_words", C.c_int, [C.c_int64, _vp, C.c_uint64, _vp, _vp]),
@@ -169,6 +173,34 @@ def dpd_set_species(ctx, a, gamma):
         raise ValueError("a and gamma must be square and of equal size")
     _check(ctx, load().dpd_set_species(ctx, ns, a.ctypes.data_as(_P(C.c_double)),
                                        gamma.ctypes.data_as(_P(C.c_double))))
+
+
+def dpd_set_walls(ctx, walls):
+    """walls: list of (type, (p0, p1, p2, p3), (uwx, uwy, uwz)) -- see dpd.h (NEXT-3)."""
+    walls = list(walls or [])
+    t = np.array([w[0] for w in walls], np.int32)
+    prm = np.array([list(w[1]) for w in walls], np.float64).reshape(-1)
+    uw = np.array([list(w[2]) for w in walls], np.float64).reshape(-1)
+    _check(ctx, load().dpd_set_walls(ctx, len(walls), _ptr(t) if len(walls) else None,
+                                     _ptr(prm) if len(walls) else None, _ptr(uw) if len(walls) else None))
+
+
+def dpd_set_frozen_species(ctx, mask):
+    _check(ctx, load().dpd_set_frozen_species(ctx, int(mask)))
+
+
+def dpd_wall_carve(ctx, wall_species):
+    """Frozen layer + removal; returns (n_frozen, n_removed) of this context."""
+    nf, nr = C.c_int64(), C.c_int64()
+    _check(ctx, load().dpd_wall_carve(ctx, int(wall_species), C.byref(nf), C.byref(nr)))
+    return nf.value, nr.value
+
+
+def dpd_wall_sdf(ctx, x):
+    x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)
+    out = np.empty(len(x), np.float32)
+    _check(ctx, load().dpd_wall_sdf(ctx, len(x), _ptr(x), _ptr(out)))
+    return out
 
 
 def dpd_step(ctx, nsteps):

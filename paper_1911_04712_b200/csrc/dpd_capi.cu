@@ -80,6 +80,14 @@ struct DevBuf {
     }
 };
 
+template <class T>
+struct ScopedBuf : DevBuf<T> {
+    ScopedBuf() = default;
+    ScopedBuf(const ScopedBuf &) = delete;
+    ScopedBuf &operator=(const ScopedBuf &) = delete;
+    ~ScopedBuf() { this->release(); }
+};
+
 struct PendingTiming {
     cudaEvent_t a, b;
     int kid;
@@ -104,6 +112,12 @@ struct dpd_ctx {
     double body_f = 0.0;
     int kmode = 2;
     int nspecies = 1;   // NEXT-2 species matrix size (kmode 3 when > 1)
+    int body_mode = 0;  // 0: periodic Poiseuille, 1: uniform +f along z
+    int frozen_mask = 0; // NEXT-3: species that never move (frozen wall layer)
+    int nwall = 0;       // NEXT-3 SDF primitives (global frame)
+    int wtype[DPD_MAX_WALLS] = {0};
+    float wprm[DPD_MAX_WALLS][4] = {};
+    float wvel[DPD_MAX_WALLS][3] = {};
     int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel, 2: cell-warp
     Geom geom{};
     PairP pp{};
@@ -294,11 +308,20 @@ int ensure_capacity(dpd_ctx *c, int64_t n)
 
 IntegP integ(const dpd_ctx *c, float dt_drift, float kick)
 {
-    IntegP ip;
+    IntegP ip{};
     ip.dt = dt_drift;
     ip.kick = kick;
     ip.body_f = (float)c->body_f;
     ip.x_half = (float)(0.5 * c->box[0] - c->origin[0]);
+    ip.body_mode = c->body_mode;
+    ip.frozen_mask = c->frozen_mask;
+    ip.nwall = c->nwall;
+    for (int k = 0; k < DPD_MAX_WALLS; ++k) {
+        ip.wtype[k] = c->wtype[k];
+        for (int q = 0; q < 4; ++q) ip.wprm[k][q] = c->wprm[k][q];
+        for (int q = 0; q < 3; ++q) ip.wvel[k][q] = c->wvel[k][q];
+    }
+    for (int k = 0; k < 3; ++k) ip.origin[k] = c->origin[k];
     return ip;
 }
 
@@ -979,6 +1002,11 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
         c->force_impl = (int)value;
         return DPD_OK;
     }
+    if (strcmp(name, "body_force_mode") == 0) {
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "body_force_mode must be 0 or 1");
+        c->body_mode = (int)value;
+        return DPD_OK;
+    }
     if (strcmp(name, "row_pruning") == 0) {
         if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "row_pruning must be 0 or 1");
         c->fix.prune = (int)value;
@@ -1046,6 +1074,130 @@ int dpd_set_species(dpd_ctx *c, int nspecies, const double *a, const double *gam
     c->nspecies = ns;
     c->kmode = (ns > 1) ? 3 : ((c->power == 0.5) ? 0 : (c->power == 1.0 ? 1 : 2));
     set_fixed_scale(c, amax, gmax);
+    return DPD_OK;
+}
+
+int dpd_set_walls(dpd_ctx *c, int nprim, const int32_t *type, const double *prm, const double *uw)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (nprim < 0 || nprim > DPD_MAX_WALLS) return fail(c, DPD_ERR_ARG, "nprim must be in [0, %d]", DPD_MAX_WALLS);
+    if (nprim > 0 && (!type || !prm || !uw)) return fail(c, DPD_ERR_ARG, "null wall arrays");
+    for (int k = 0; k < nprim; ++k) {
+        const double *q = prm + 4 * k;
+        for (int t = 0; t < 4; ++t)
+            if (!std::isfinite(q[t])) return fail(c, DPD_ERR_CONFIG, "wall %d: non-finite parameter", k);
+        for (int t = 0; t < 3; ++t)
+            if (!std::isfinite(uw[3 * k + t])) return fail(c, DPD_ERR_CONFIG, "wall %d: non-finite velocity", k);
+        if (type[k] == 1) {
+            const double nn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2]);
+            if (std::fabs(nn - 1.0) > 1e-6) return fail(c, DPD_ERR_CONFIG, "wall %d: plane normal must be unit", k);
+        } else if (type[k] >= 2 && type[k] <= 4) {
+            if (!(q[2] > 0.0) || std::fabs(std::fabs(q[3]) - 1.0) != 0.0)
+                return fail(c, DPD_ERR_CONFIG, "wall %d: cylinder needs R > 0 and sign +-1", k);
+        } else {
+            return fail(c, DPD_ERR_CONFIG, "wall %d: unknown type %d", k, (int)type[k]);
+        }
+    }
+    c->nwall = nprim;
+    for (int k = 0; k < DPD_MAX_WALLS; ++k) {
+        c->wtype[k] = k < nprim ? type[k] : 0;
+        for (int t = 0; t < 4; ++t) c->wprm[k][t] = k < nprim ? (float)prm[4 * k + t] : 0.0f;
+        for (int t = 0; t < 3; ++t) c->wvel[k][t] = k < nprim ? (float)uw[3 * k + t] : 0.0f;
+    }
+    return DPD_OK;
+}
+
+int dpd_set_frozen_species(dpd_ctx *c, int32_t mask)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (mask < 0) return fail(c, DPD_ERR_ARG, "mask must be >= 0");
+    c->frozen_mask = mask;
+    return DPD_OK;
+}
+
+int dpd_wall_sdf(dpd_ctx *c, int64_t n, const float *x, float *sdf)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (n < 0 || (n > 0 && (!x || !sdf))) return fail(c, DPD_ERR_ARG, "bad arguments");
+    if (n == 0) return DPD_OK;
+    TRY(sync_check(c));
+    CUDA_TRY(c, c->stage.reserve((size_t)n * 4));
+    float *dx = c->stage.p, *ds = c->stage.p + 3 * n;
+    CUDA_TRY(c, cudaMemcpyAsync(dx, x, sizeof(float) * 3 * n, cudaMemcpyDefault, c->stream));
+    IntegP ip = integ(c, 0.0f, 0.0f);
+    ip.origin[0] = ip.origin[1] = ip.origin[2] = 0.0f; // x is global
+    TRY(launch(c, KID_DEBUG, [&] { k_wall_sdf_eval<<<nblk(n, 256), 256, 0, c->stream>>>(dx, (int)n, ip, ds); }));
+    CUDA_TRY(c, cudaMemcpyAsync(sdf, ds, sizeof(float) * n, cudaMemcpyDefault, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return DPD_OK;
+}
+
+int dpd_wall_carve(dpd_ctx *c, int32_t wall_species, int64_t *n_frozen, int64_t *n_removed)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (wall_species < 0 || wall_species > 30 || (c->nspecies > 1 && wall_species >= c->nspecies))
+        return fail(c, DPD_ERR_ARG, "wall species %d out of range", (int)wall_species);
+    TRY(sync_check(c));
+    if (c->need_prime) return fail(c, DPD_ERR_ARG, "group members must be primed (dpd_group_step(.., 0)) first");
+    const int n = (int)c->n;
+    const int b = c->cur, o = 1 - c->cur;
+    ScopedBuf<int> keep, cnt, kbid, nid, epoch; // freed on every return path
+    ScopedBuf<unsigned long long> tstate;
+    CUDA_TRY(c, keep.reserve((size_t)std::max(n, 1)));
+    CUDA_TRY(c, cnt.reserve(2));
+    CUDA_TRY(c, cudaMemsetAsync(cnt.p, 0, 2 * sizeof(int), c->stream));
+    const bool renumber = c->dense_ids && !c->dist && n > 0;
+    if (renumber) {
+        CUDA_TRY(c, kbid.reserve((size_t)n));
+        CUDA_TRY(c, nid.reserve((size_t)n + 1));
+        const size_t tiles = (size_t)(n + kScanTile - 1) / kScanTile;
+        CUDA_TRY(c, tstate.reserve(tiles));
+        CUDA_TRY(c, epoch.reserve(1));
+        CUDA_TRY(c, cudaMemsetAsync(tstate.p, 0, tiles * sizeof(unsigned long long), c->stream));
+        CUDA_TRY(c, cudaMemsetAsync(epoch.p, 0, sizeof(int), c->stream));
+    }
+    const IntegP ip = integ(c, 0.0f, 0.0f);
+    const float hk = c->primed ? 0.0f : (float)(0.5 * c->dt); // stored u -> full-step v
+    int hc[2] = {0, 0};
+    if (n > 0) {
+        TRY(launch(c, KID_GATHER, [&] {
+            k_wall_classify<<<nblk(n, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, n, ip, hk,
+                                                                 (float)c->rc, wall_species, keep.p, cnt.p);
+        }));
+        CUDA_TRY(c, cudaMemsetAsync(count_ptr(c), 0, sizeof(int), c->stream));
+        TRY(launch(c, KID_GATHER, [&] {
+            k_wall_compact<<<nblk(n, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, n, keep.p, c->pos[o].p,
+                                                                c->vel[o].p, c->frc[o].p, count_ptr(c),
+                                                                renumber ? kbid.p : nullptr);
+        }));
+        CUDA_TRY(c, cudaMemcpyAsync(hc, cnt.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        c->cur = o;
+        TRY(sync_check(c));
+        if (renumber && hc[1] > 0) {
+            const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
+            TRY(launch(c, KID_GATHER, [&] {
+                k_scan<<<tiles, kScanThreads, 0, c->stream>>>(kbid.p, nid.p, n, tstate.p,
+                                                              reinterpret_cast<unsigned *>(epoch.p));
+            }));
+            TRY(launch(c, KID_GATHER, [&] {
+                k_renumber<<<nblk(c->n, 256), 256, 0, c->stream>>>(c->pos[c->cur].p, (int)c->n, nid.p);
+            }));
+        }
+    }
+    c->frozen_mask |= 1 << wall_species;
+    // re-sort the survivors into cells (dt = 0) and prime F at the current step (C-2 item 2)
+    const IntegP ip0 = integ(c, 0.0f, 0.0f);
+    TRY(phase_bin(c, ip0, false));
+    TRY(phase_sort(c, ip0, false));
+    c->primed = true;
+    if (c->group) {
+        c->need_prime = true;
+    } else {
+        TRY(prime_one(c));
+    }
+    TRY(sync_check(c));
+    if (n_frozen) *n_frozen = hc[0];
+    if (n_removed) *n_removed = hc[1];
     return DPD_OK;
 }
 
@@ -1218,11 +1370,11 @@ static int gather(dpd_ctx *c, float *pos, float *vel, float *f, int by_id)
     float *d_f = f ? c->stage.p + 6 * (size_t)cnt : nullptr;
     const float hk = c->primed ? 0.0f : (float)(0.5 * c->dt);
     const int b = c->cur;
-    const float x_half = (float)(0.5 * c->box[0] - c->origin[0]);
+    const IntegP ip = integ(c, 0.0f, 0.0f);
     const float3 org = make_float3(c->origin[0], c->origin[1], c->origin[2]);
     TRY(launch(c, KID_GATHER, [&] {
-        k_gather_id<<<nblk(cnt, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, (int)cnt, hk,
-                                                           (float)c->body_f, x_half, org, d_pos, d_vel, d_f, by_id);
+        k_gather_id<<<nblk(cnt, 256), 256, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, (int)cnt, hk, ip,
+                                                           org, d_pos, d_vel, d_f, by_id);
     }));
     if (pos) CUDA_TRY(c, cudaMemcpyAsync(pos, d_pos, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));
     if (vel) CUDA_TRY(c, cudaMemcpyAsync(vel, d_vel, sizeof(float) * 3 * cnt, cudaMemcpyDefault, c->stream));

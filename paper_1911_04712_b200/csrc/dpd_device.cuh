@@ -45,11 +45,21 @@ struct PairP {
 };
 
 // Integrator parameters (C-2 item 3 / C-6).
+constexpr int DPD_MAX_WALLS = 4;
+
 struct IntegP {
     float dt;       // drift time step (0 when only re-binning at set time)
     float kick;     // velocity kick factor: dt/2 on the first step after set, dt after
-    float body_f;   // periodic-Poiseuille magnitude f
+    float body_f;   // body-force magnitude f
     float x_half;   // global L_x / 2 expressed in local coordinates
+    int body_mode;  // 0: periodic Poiseuille (sign flips at L_x/2), 1: uniform +f along z
+    int frozen_mask; // species s never moves iff bit s (NEXT-3 frozen wall layer)
+    // SDF walls (NEXT-3, C-23): solid = union of primitives, s = max_k s_k > 0 inside
+    int nwall;
+    int wtype[DPD_MAX_WALLS];      // 1 plane s = n.x - c; 2/3/4 cylinder along x/y/z
+    float wprm[DPD_MAX_WALLS][4];  // plane (nx, ny, nz, c); cylinder (c1, c2, R, sign)
+    float wvel[DPD_MAX_WALLS][3];  // translational wall velocity
+    float origin[3];               // local -> global coordinates (walls are global)
 };
 
 // ---------------------------------------------------------------------------------------

@@ -44,19 +44,87 @@ __device__ __forceinline__ int cell_index(const Geom &g, float x, float y, float
     return ix + g.ext[0] * (iy + g.ext[1] * iz);
 }
 
+// Body force along z: periodic Poiseuille, or uniform (wall-bounded flows).
+__device__ __forceinline__ float body_fz(const IntegP &ip, float x_local)
+{
+    if (ip.body_mode == 1) return ip.body_f;
+    return (x_local <= ip.x_half) ? -ip.body_f : ip.body_f;
+}
+
+__device__ __forceinline__ bool is_frozen(const IntegP &ip, const float4 v)
+{
+    return (ip.frozen_mask >> (__float_as_int(v.w) & 31)) & 1;
+}
+
+// Wall SDF at a local-frame point (C-23): s = max over primitives of the signed distance
+// (global frame), *arg = the maximising primitive.  Fixed _rn arithmetic: k_bin and
+// k_scatter must take the same bounce decisions.
+__device__ __forceinline__ float wall_sdf(const IntegP &ip, float x, float y, float z, int &arg)
+{
+    const float g[3] = {__fadd_rn(x, ip.origin[0]), __fadd_rn(y, ip.origin[1]), __fadd_rn(z, ip.origin[2])};
+    float best = -3.0e38f;
+    arg = 0;
+    for (int k = 0; k < ip.nwall; ++k) {
+        const float *q = ip.wprm[k];
+        float sk;
+        if (ip.wtype[k] == 1) {
+            sk = __fsub_rn(__fmaf_rn(q[2], g[2], __fmaf_rn(q[1], g[1], __fmul_rn(q[0], g[0]))), q[3]);
+        } else {
+            const int ax = ip.wtype[k] - 2, a = (ax + 1) % 3, b = (ax + 2) % 3;
+            const float da = __fsub_rn(g[a], q[0]), db = __fsub_rn(g[b], q[1]);
+            sk = __fmul_rn(q[3], __fsub_rn(q[2], __fsqrt_rn(__fmaf_rn(da, da, __fmul_rn(db, db)))));
+        }
+        if (sk > best) {
+            best = sk;
+            arg = k;
+        }
+    }
+    return best;
+}
+
 // First half of GW-VV fused with the previous step's second half (C-6):
 //   u' = u + kick (F + f_body(x));  x' = wrap(x + dt u')
-// Explicit _rn intrinsics pin the rounding so k_bin and k_scatter agree bit-for-bit.
+// with bounce-back off SDF walls (C-23): if x' is inside the solid, bisection
+// (32 halvings) finds the last point x + t u with s <= 0, the particle is placed there and
+// u' <- 2 u_w - u'.  Frozen species do not move.  Explicit _rn intrinsics pin the rounding
+// so k_bin and k_scatter agree bit-for-bit.
 __device__ __forceinline__ void advance(const Geom &g, const IntegP &ip, const float4 p, const float4 v,
                                         const float4 f, float3 &xn, float3 &un)
 {
-    const float fb = (p.x <= ip.x_half) ? -ip.body_f : ip.body_f;
+    if (ip.frozen_mask && is_frozen(ip, v)) {
+        un = make_float3(v.x, v.y, v.z);
+        xn = make_float3(p.x, p.y, p.z);
+        return;
+    }
+    const float fb = body_fz(ip, p.x);
     un.x = __fmaf_rn(ip.kick, f.x, v.x);
     un.y = __fmaf_rn(ip.kick, f.y, v.y);
     un.z = __fmaf_rn(ip.kick, __fadd_rn(f.z, fb), v.z);
     xn.x = __fmaf_rn(ip.dt, un.x, p.x);
     xn.y = __fmaf_rn(ip.dt, un.y, p.y);
     xn.z = __fmaf_rn(ip.dt, un.z, p.z);
+    if (ip.nwall > 0) {
+        int arg;
+        if (wall_sdf(ip, xn.x, xn.y, xn.z, arg) > 0.0f) {
+            float lo = 0.0f, hi = ip.dt;
+            if (wall_sdf(ip, p.x, p.y, p.z, arg) > 0.0f) hi = 0.0f; // already inside: stay, reverse
+            for (int it = 0; it < 32 && hi > 0.0f; ++it) {
+                const float mid = __fmul_rn(0.5f, __fadd_rn(lo, hi));
+                if (wall_sdf(ip, __fmaf_rn(mid, un.x, p.x), __fmaf_rn(mid, un.y, p.y), __fmaf_rn(mid, un.z, p.z),
+                             arg) > 0.0f)
+                    hi = mid;
+                else
+                    lo = mid;
+            }
+            xn.x = __fmaf_rn(lo, un.x, p.x);
+            xn.y = __fmaf_rn(lo, un.y, p.y);
+            xn.z = __fmaf_rn(lo, un.z, p.z);
+            wall_sdf(ip, xn.x, xn.y, xn.z, arg);
+            un.x = __fsub_rn(2.0f * ip.wvel[arg][0], un.x);
+            un.y = __fsub_rn(2.0f * ip.wvel[arg][1], un.y);
+            un.z = __fsub_rn(2.0f * ip.wvel[arg][2], un.z);
+        }
+    }
     if (!g.split[0]) xn.x = wrap_coord(xn.x, g.L[0]);
     if (!g.split[1]) xn.y = wrap_coord(xn.y, g.L[1]);
     if (!g.split[2]) xn.z = wrap_coord(xn.z, g.L[2]);
@@ -468,7 +536,7 @@ __global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ po
 // ---------------------------------------------------------------------------------------
 // Full-step velocity v = u + hk (F + f_body(x)), hk = kick_next - dt/2 (0 right after set).
 __global__ void k_gather_id(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                            const float4 *__restrict__ frc, int n, float hk, float body_f, float x_half,
+                            const float4 *__restrict__ frc, int n, float hk, IntegP ip,
                             float3 origin, float *__restrict__ pos3, float *__restrict__ vel3,
                             float *__restrict__ f3, int by_id)
 {
@@ -482,10 +550,11 @@ __global__ void k_gather_id(const float4 *__restrict__ pos, const float4 *__rest
         pos3[3 * row + 2] = p.z + origin.z;
     }
     if (vel3) {
-        const float fb = (p.x <= x_half) ? -body_f : body_f;
-        vel3[3 * row + 0] = __fmaf_rn(hk, f.x, v.x);
-        vel3[3 * row + 1] = __fmaf_rn(hk, f.y, v.y);
-        vel3[3 * row + 2] = __fmaf_rn(hk, __fadd_rn(f.z, fb), v.z);
+        const float fb = body_fz(ip, p.x);
+        const float h = (ip.frozen_mask && is_frozen(ip, v)) ? 0.0f : hk; // frozen: the wall velocity
+        vel3[3 * row + 0] = __fmaf_rn(h, f.x, v.x);
+        vel3[3 * row + 1] = __fmaf_rn(h, f.y, v.y);
+        vel3[3 * row + 2] = __fmaf_rn(h, __fadd_rn(f.z, fb), v.z);
     }
     if (f3) {
         f3[3 * row + 0] = f.x;
@@ -503,6 +572,78 @@ __global__ void k_ids_cells(const float4 *__restrict__ pos, int n, Geom g, int32
     const int id = __float_as_int(p.w);
     if (ids) ids[i] = id;
     if (cell_of_id) cell_of_id[id] = cell_index(g, p.x, p.y, p.z);
+}
+
+// ---------------------------------------------------------------------------------------
+// NEXT-3 walls: frozen-layer carve (C-23).  s > r_c: removed; 0 < s <= r_c:
+// frozen wall particle of species wall_species with the wall velocity; else fluid, whose
+// stored half-step velocity is first completed to the full-step v = u + hk (F + f_body).
+// ---------------------------------------------------------------------------------------
+__global__ void k_wall_classify(float4 *__restrict__ pos, float4 *__restrict__ vel, const float4 *__restrict__ frc,
+                                int n, IntegP ip, float hk, float rc, int wall_species, int *__restrict__ keep,
+                                int *counters)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = pos[i];
+    float4 v = vel[i];
+    int arg;
+    const float sd = wall_sdf(ip, p.x, p.y, p.z, arg);
+    int k = 1;
+    if (ip.frozen_mask && is_frozen(ip, v)) {
+        // an existing wall particle stays as it is
+    } else if (sd > rc) {
+        k = 0;
+        atomicAdd(&counters[1], 1);
+    } else if (sd > 0.0f) {
+        v = make_float4(ip.wvel[arg][0], ip.wvel[arg][1], ip.wvel[arg][2], __int_as_float(wall_species));
+        atomicAdd(&counters[0], 1);
+    } else {
+        const float4 f = frc[i];
+        v.x = __fmaf_rn(hk, f.x, v.x);
+        v.y = __fmaf_rn(hk, f.y, v.y);
+        v.z = __fmaf_rn(hk, __fadd_rn(f.z, body_fz(ip, p.x)), v.z);
+    }
+    vel[i] = v;
+    keep[i] = k;
+}
+
+// Compaction of the kept particles (order is irrelevant: they are re-sorted into cells).
+__global__ void k_wall_compact(const float4 *__restrict__ pos, const float4 *__restrict__ vel, int n,
+                               const int *__restrict__ keep, float4 *__restrict__ pos_o, float4 *__restrict__ vel_o,
+                               float4 *__restrict__ frc_o, int *n_out, int *__restrict__ keep_by_id)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool k = i < n && keep[i];
+    if (i < n && keep_by_id) keep_by_id[__float_as_int(pos[i].w)] = k ? 1 : 0;
+    const unsigned m = __ballot_sync(0xffffffffu, k);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(n_out, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (k) {
+        const int slot = base + __popc(m & lanemask_lt());
+        pos_o[slot] = pos[i];
+        vel_o[slot] = vel[i];
+        frc_o[slot] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+}
+
+// Dense renumbering after a carve (single domain): id <- rank of id among the kept ids.
+__global__ void k_renumber(float4 *__restrict__ pos, int n, const int *__restrict__ new_id)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    pos[i].w = __int_as_float(new_id[__float_as_int(pos[i].w)]);
+}
+
+// Wall SDF at global points (test hook for the device SDF).
+__global__ void k_wall_sdf_eval(const float *__restrict__ x3, int n, IntegP ip, float *__restrict__ s)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int arg;
+    s[i] = wall_sdf(ip, x3[3 * i], x3[3 * i + 1], x3[3 * i + 2], arg);
 }
 
 // Species index (vel.w, NEXT-2) per particle, in id order (by_id) or storage order.
