@@ -750,6 +750,10 @@ int setup_geometry(dpd_ctx *c, const double len[3], const int split[3])
 // gamma in use: bound a single pair's force magnitude by a + 6.7 sigma/sqrt(dt) (|xi| <= 6.66
 // with 32-bit u1) + 20 gamma max(1, sqrt(kT)) (relative speed), keep |f scale| < 2^21;
 // larger magnitudes are detected on the device and reported as DPD_ERR_NUMERIC.
+// sqrt(2 ln 2): the device pair paths use box_muller_s = xi / sqrt(2 ln 2) and fold the
+// constant into sigma/sqrt(dt) here (PairP::sig_dt, PairP::ss)
+constexpr double kBMd = 1.1774100225154747;
+
 void set_fixed_scale(dpd_ctx *c, double amax, double gmax)
 {
     const double sig_dt = std::sqrt(2.0 * gmax * c->kT) / std::sqrt(c->dt);
@@ -782,7 +786,7 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     PairP pp{};
     pp.a = (float)a;
     pp.gamma = (float)gamma;
-    pp.sig_dt = (float)(std::sqrt(2.0 * gamma * kT) / std::sqrt(dt));
+    pp.sig_dt = (float)(std::sqrt(2.0 * gamma * kT) / std::sqrt(dt) * kBMd); // x sqrt(2 ln 2): box_muller_s
     pp.sa[0] = pp.a; // one species until dpd_set_species
     pp.sg[0] = pp.gamma;
     pp.ss[0] = pp.sig_dt;
@@ -1062,7 +1066,7 @@ int dpd_set_species(dpd_ctx *c, int nspecies, const double *a, const double *gam
             const double gv = gamma[i * ns + j];
             pp.sa[t] = (float)a[i * ns + j];
             pp.sg[t] = (float)gv;
-            pp.ss[t] = (float)(std::sqrt(2.0 * gv * c->kT) / std::sqrt(c->dt)); // FDT per pair
+            pp.ss[t] = (float)(std::sqrt(2.0 * gv * c->kT) / std::sqrt(c->dt) * kBMd); // FDT per pair
         }
     if (ns == 1) {
         c->a = a[0];

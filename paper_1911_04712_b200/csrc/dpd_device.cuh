@@ -32,7 +32,7 @@ constexpr int DPD_MAX_SPECIES = 4;
 struct PairP {
     float a;        // conservative amplitude
     float gamma;    // dissipative coefficient
-    float sig_dt;   // sigma / sqrt(dt), sigma = sqrt(2 gamma kT)            (C-3)
+    float sig_dt;   // sigma / sqrt(dt) * kBM, sigma = sqrt(2 gamma kT)      (C-3; kBM below)
     float inv_rc;   // 1 / r_c
     float rc2;      // r_c^2
     float power;    // k (w_R = w^k)                                         (C-4)
@@ -41,7 +41,7 @@ struct PairP {
     // pair's a, gamma and sigma/sqrt(dt); ti, tj travel in vel.w
     float sa[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
     float sg[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
-    float ss[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
+    float ss[DPD_MAX_SPECIES * DPD_MAX_SPECIES]; // x kBM like sig_dt
 };
 
 // Integrator parameters (C-2 item 3 / C-6).
@@ -103,14 +103,21 @@ __device__ __forceinline__ float sqrt_approx(float x)
 // Box-Muller (C-7): u1 = (w0 + 1) 2^-32 in (0, 1], u2 = w1 2^-32;
 // xi = sqrt(-2 ln u1) cos(2 pi u2).  cos is evaluated on the signed image of u2 in
 // [-1/2, 1/2) so the fast cosine sees |arg| <= pi.
-__device__ __forceinline__ float box_muller(uint32_t w0, uint32_t w1)
+// box_muller_s returns xi / kBM with kBM = sqrt(2 ln 2): -2 ln u1 = 2 ln 2 (-log2 u1), so the
+// constant leaves the per-pair path and is folded into sigma/sqrt(dt) on the host (PairP).
+constexpr float kBM = 1.1774100225154747f; // sqrt(2 ln 2)
+
+__device__ __forceinline__ float box_muller_s(uint32_t w0, uint32_t w1)
 {
     const float two_m32 = 2.3283064365386963e-10f; // 2^-32
     const float u1 = __fmaf_rn(__uint2float_rn(w0), two_m32, two_m32);
-    const float m2ln = -2.0f * __logf(u1);
-    const float rad = sqrt_approx(fmaxf(m2ln, 0.0f));
-    const float u2s = __int2float_rn((int)w1) * two_m32;
-    return rad * __cosf(6.283185307179586f * u2s);
+    const float rad = sqrt_approx(fmaxf(-__log2f(u1), 0.0f));
+    return rad * __cosf(__int2float_rn((int)w1) * (6.283185307179586f * two_m32));
+}
+
+__device__ __forceinline__ float box_muller(uint32_t w0, uint32_t w1)
+{
+    return kBM * box_muller_s(w0, w1);
 }
 
 // w_R for the kernel exponent k (C-4): k = 1/2 -> sqrt(w); k = 1 -> w; else w^k.
@@ -122,17 +129,19 @@ __device__ __forceinline__ float weight_R(float w, float k)
     else return w > 0.0f ? exp2f(k * __log2f(w)) : 0.0f; // 2 (generic k) and 3 (species matrix)
 }
 
-// Scalar pair force along d = r_i - r_j: returns s such that f_ij = s * d.
+// Scalar pair force along d = r_i - r_j: returns s such that f_ij = s * d, and
+// the force magnitude mag (for the fixed-point range check of the tiled kernel).
 //   mag = a w - gamma w_D (e . v_ij) + sigma/sqrt(dt) w_R xi ;  s = mag / r
 // r2 in (0, rc2) assumed.  KMODE 0: k = 1/2, 1: k = 1, 2: generic k, 3: generic k with the
-// species matrix (a, gamma, sigma of the pair looked up from the species in vel.w).
+// species matrix (a, gamma, sigma of the pair looked up from the species ti, tj).
+// pp.sig_dt / pp.ss hold sigma/sqrt(dt) * kBM (box_muller_s convention).
 template <int KMODE>
-__device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
-                                             uint32_t ks, float vwi, float vwj)
+__device__ __forceinline__ float pair_mag(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
+                                          uint32_t ks, int ti, int tj, float &mag)
 {
     float a = pp.a, gamma = pp.gamma, sig_dt = pp.sig_dt;
     if constexpr (KMODE == 3) {
-        const int t = __float_as_int(vwi) * DPD_MAX_SPECIES + __float_as_int(vwj);
+        const int t = ti * DPD_MAX_SPECIES + tj;
         a = pp.sa[t];
         gamma = pp.sg[t];
         sig_dt = pp.ss[t];
@@ -141,11 +150,21 @@ __device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dv
     const float r = r2 * rinv;
     const float w = fmaxf(__fmaf_rn(-r, pp.inv_rc, 1.0f), 0.0f);
     const float wR = weight_R<KMODE>(w, pp.power);
-    const float wD = (KMODE == 0) ? w : wR * wR;
     const uint2 wd = pair_words(idi, idj, ks);
-    const float xi = box_muller(wd.x, wd.y);
-    const float mag = a * w - gamma * wD * (dvdot * rinv) + sig_dt * wR * xi;
+    const float xr = box_muller_s(wd.x, wd.y) * wR;
+    float cons;
+    if constexpr (KMODE == 0) cons = w * __fmaf_rn(-gamma, dvdot * rinv, a); // w_D = w_R^2 = w
+    else cons = __fmaf_rn(a, w, -gamma * (wR * wR) * (dvdot * rinv));
+    mag = __fmaf_rn(xr, sig_dt, cons);
     return mag * rinv;
+}
+
+template <int KMODE>
+__device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
+                                             uint32_t ks, float vwi, float vwj)
+{
+    float mag;
+    return pair_mag<KMODE>(pp, r2, dvdot, idi, idj, ks, __float_as_int(vwi), __float_as_int(vwj), mag);
 }
 
 // Cell coordinate along one dimension (C-8): min((int)(x * inv_h), n - 1), fp32 product.

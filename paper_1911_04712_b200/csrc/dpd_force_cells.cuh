@@ -48,6 +48,41 @@ __device__ __forceinline__ float4 ldp_c(const ForceCellSmem &S, int j)
     return make_float4(S.sx[j], S.sy[j], S.sz[j], __int_as_float(S.sid[j]));
 }
 
+// Pair force in the global-memory convention (pi.w = id bits, vi.w = species bits):
+// f_ij = s (dx, dy, dz), s = 0 for coincident particles (C-11).
+template <int KMODE>
+__device__ __forceinline__ float pair_core_c(const PairP &pp, float4 pi, float4 vi, float4 pj, float4 vj,
+                                             uint32_t ks, float &dx, float &dy, float &dz)
+{
+    dx = pi.x - pj.x;
+    dy = pi.y - pj.y;
+    dz = pi.z - pj.z;
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
+    const float s = pair_scalar<KMODE>(pp, fmaxf(r2, 1e-30f), dvdot, (uint32_t)__float_as_int(pi.w),
+                                       (uint32_t)__float_as_int(pj.w), ks, vi.w, vj.w);
+    return r2 > 0.0f ? s : 0.0f;
+}
+
+// Range check of the fixed-point conversion and (debug) pair recording.
+template <bool RECORD>
+__device__ __forceinline__ void pair_checks_c(const PairP &pp, const FixP &fx, float4 pi, float4 pj, float s,
+                                              float dx, float dy, float dz, uint32_t ks, PairRec &rec, int *err)
+{
+    const float r2 = dx * dx + dy * dy + dz * dz;
+    if (fabsf(s) * (r2 * rsqrtf(fmaxf(r2, 1e-30f))) > fx.mag_lim) raise_err(err, ERR_RANGE, __float_as_int(pi.w));
+    if constexpr (RECORD) {
+        if (r2 > 0.0f) {
+            const uint32_t idi = (uint32_t)__float_as_int(pi.w), idj = (uint32_t)__float_as_int(pj.w);
+            const unsigned long long k = atomicAdd(rec.count, 1ull);
+            if ((long long)k < rec.cap) {
+                const uint2 wd = pair_words(idi, idj, ks);
+                rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
+            }
+        }
+    }
+}
+
 // Strided sweep of [lo, hi): this lane takes the aligned candidate pairs (2m, 2m + 1) with
 // m = m0 + q, m0 + q + Q, ... (m0 = lo / 2), appending at most `room` hits.  Returns the
 // first candidate index it did not examine (hi if done) -- only relevant when the list
@@ -118,8 +153,8 @@ __device__ __forceinline__ void warp_pairs(ForceCellSmem &S, int lane, int warp,
             const int j = S.lst[lrow + t];
             const float4 pj = ldp_c(S, j);
             float dx, dy, dz;
-            const float s = pair_core<KMODE>(pp, pi, vi, pj, S.sv[j], ks, dx, dy, dz);
-            pair_checks<RECORD>(pp, fx, pi, pj, s, dx, dy, dz, ks, rec, err);
+            const float s = pair_core_c<KMODE>(pp, pi, vi, pj, S.sv[j], ks, dx, dy, dz);
+            pair_checks_c<RECORD>(pp, fx, pi, pj, s, dx, dy, dz, ks, rec, err);
             const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
                       qz = to_fixed(s * dz, fx.scale);
             fxi += qx;
@@ -314,8 +349,8 @@ __global__ void __launch_bounds__(FC_NTHR, 3)
                             if (!(ddx * ddx + ddy * ddy + ddz * ddz < pp.rc2)) continue;
                             const float4 pj = ldp_c(S, jj);
                             float dx, dy, dz;
-                            const float s = pair_core<KMODE>(pp, pi, vi, pj, S.sv[jj], ks, dx, dy, dz);
-                            pair_checks<RECORD>(pp, fx, pi, pj, s, dx, dy, dz, ks, rec, err);
+                            const float s = pair_core_c<KMODE>(pp, pi, vi, pj, S.sv[jj], ks, dx, dy, dz);
+                            pair_checks_c<RECORD>(pp, fx, pi, pj, s, dx, dy, dz, ks, rec, err);
                             const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
                                       qz = to_fixed(s * dz, fx.scale);
                             atomicAdd(&S.acc[0][s_i], qx);

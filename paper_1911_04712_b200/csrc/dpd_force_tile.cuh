@@ -47,11 +47,10 @@ struct FixP {
 };
 
 struct ForceTileSmem {
-    float4 sv[FT_SCAP];                       // staged velocities (w: species)
+    float4 sv[FT_SCAP];                       // staged velocities; w: id bits | species << 30 (stage_fix)
     unsigned short lst[FT_NTHR * FT_LSTRIDE]; // per-thread pair lists (one home particle each);
                                               // during staging: the AoS landing buffer of the positions
     float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // staged positions (tile frame), SoA
-    int sid[FT_SCAP];                            // staged ids
     int acc[3][FT_SCAP];                         // fixed-point force sums
     int woex[FT_NWARP * FT_WSTRIDE];             // per warp: compacted owners' list prefix (+ total)
     int wsi[FT_NWARP * FT_WSTRIDE];              //   staged index of the owner
@@ -80,10 +79,32 @@ static_assert(offsetof(ForceTileSmem, lst) % 16 == 0 && offsetof(ForceTileSmem, 
                   offsetof(ForceTileSmem, sy) % 8 == 0 && offsetof(ForceTileSmem, sz) % 8 == 0,
               "cp.async / packed-pair alignment");
 
-// Staged position j as (x, y, z, id bits).
+// The staged velocity word w carries the particle's id (and, for the species matrix, its
+// species in bits 30-31; ids stay below 2^30), so one LDS.128 fetches velocity and id.
+template <int KMODE>
+__device__ __forceinline__ uint32_t w_id(float w)
+{
+    return KMODE == 3 ? (__float_as_uint(w) & 0x3FFFFFFFu) : __float_as_uint(w);
+}
+
+__device__ __forceinline__ int w_species(float w)
+{
+    return (int)(__float_as_uint(w) >> 30);
+}
+
+// Staged particle j in the global-memory convention: position (x, y, z, id bits) and
+// velocity (u_x, u_y, u_z, species bits) -- cold paths (record, in-place, fallback).
+template <int KMODE>
 __device__ __forceinline__ float4 ldp(const ForceTileSmem &S, int j)
 {
-    return make_float4(S.sx[j], S.sy[j], S.sz[j], __int_as_float(S.sid[j]));
+    return make_float4(S.sx[j], S.sy[j], S.sz[j], __uint_as_float(w_id<KMODE>(S.sv[j].w)));
+}
+
+template <int KMODE>
+__device__ __forceinline__ float4 ldv(const ForceTileSmem &S, int j)
+{
+    const float4 v = S.sv[j];
+    return make_float4(v.x, v.y, v.z, __int_as_float(KMODE == 3 ? w_species(v.w) : 0));
 }
 
 __device__ __forceinline__ int to_fixed(float f, float scale)
@@ -186,7 +207,9 @@ __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__res
     }
 }
 
-// Second pass over a staged range: periodic-image shift, SoA copy, zeroed accumulators.
+// Second pass over a staged range: periodic-image shift, SoA copy, id (| species << 30) into
+// the velocity word, zeroed accumulators.
+template <int KMODE>
 __device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, float sx, float sy, float sz, int lane)
 {
     for (int k = lane; k < len; k += 32) {
@@ -195,7 +218,9 @@ __device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, flo
         S.sx[s] = p.x + sx;
         S.sy[s] = p.y + sy;
         S.sz[s] = p.z + sz;
-        S.sid[s] = __float_as_int(p.w);
+        uint32_t word = __float_as_uint(p.w);
+        if constexpr (KMODE == 3) word |= (uint32_t)__float_as_int(S.sv[s].w) << 30;
+        S.sv[s].w = __uint_as_float(word);
         S.acc[0][s] = 0;
         S.acc[1][s] = 0;
         S.acc[2][s] = 0;
@@ -240,36 +265,38 @@ __device__ __forceinline__ float pair_eval(const PairP &pp, const FixP &fx, floa
     return s;
 }
 
-// Branch-free pair force: f_ij = s (dx, dy, dz); s = 0 for coincident particles (C-11).
+// Branch-free pair force of the hot loop: f_ij = s (dx, dy, dz) for staged i (position p*,
+// velocity word vi) and staged j.  A coincident pair (r2 = 0: the idle second cursor's self
+// pair, or two particles at the same point) gets d = 0 and a finite s, hence f = 0 (C-11).
+// The largest |mag| seen is kept in amax and range-checked once per walk.
 template <int KMODE>
-__device__ __forceinline__ float pair_core(const PairP &pp, float4 pi, float4 vi, float4 pj, float4 vj, uint32_t ks,
-                                           float &dx, float &dy, float &dz)
+__device__ __forceinline__ float pair_core(const PairP &pp, float pix, float piy, float piz, float4 vi, float pjx,
+                                           float pjy, float pjz, float4 vj, uint32_t ks, float &dx, float &dy,
+                                           float &dz, float &amax)
 {
-    dx = pi.x - pj.x;
-    dy = pi.y - pj.y;
-    dz = pi.z - pj.z;
+    dx = pix - pjx;
+    dy = piy - pjy;
+    dz = piz - pjz;
     const float r2 = dx * dx + dy * dy + dz * dz;
     const float dvdot = dx * (vi.x - vj.x) + dy * (vi.y - vj.y) + dz * (vi.z - vj.z);
-    const float s = pair_scalar<KMODE>(pp, fmaxf(r2, 1e-30f), dvdot, (uint32_t)__float_as_int(pi.w),
-                                       (uint32_t)__float_as_int(pj.w), ks, vi.w, vj.w);
-    return r2 > 0.0f ? s : 0.0f;
+    float mag;
+    const float s = pair_mag<KMODE>(pp, fmaxf(r2, 1e-30f), dvdot, w_id<KMODE>(vi.w), w_id<KMODE>(vj.w), ks,
+                                    w_species(vi.w), w_species(vj.w), mag);
+    amax = fmaxf(amax, fabsf(mag));
+    return s;
 }
 
-// Range check of the fixed-point conversion and (debug) pair recording.
-template <bool RECORD>
-__device__ __forceinline__ void pair_checks(const PairP &pp, const FixP &fx, float4 pi, float4 pj, float s, float dx,
-                                            float dy, float dz, uint32_t ks, PairRec &rec, int *err)
+// Debug pair recording (RECORD instantiation only).
+template <int KMODE>
+__device__ __forceinline__ void pair_record(float4 vi, float4 vj, float dx, float dy, float dz, uint32_t ks,
+                                            PairRec &rec)
 {
-    const float r2 = dx * dx + dy * dy + dz * dz;
-    if (fabsf(s) * (r2 * rsqrtf(fmaxf(r2, 1e-30f))) > fx.mag_lim) raise_err(err, ERR_RANGE, __float_as_int(pi.w));
-    if constexpr (RECORD) {
-        if (r2 > 0.0f) {
-            const uint32_t idi = (uint32_t)__float_as_int(pi.w), idj = (uint32_t)__float_as_int(pj.w);
-            const unsigned long long k = atomicAdd(rec.count, 1ull);
-            if ((long long)k < rec.cap) {
-                const uint2 wd = pair_words(idi, idj, ks);
-                rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
-            }
+    if (dx * dx + dy * dy + dz * dz > 0.0f) {
+        const uint32_t idi = w_id<KMODE>(vi.w), idj = w_id<KMODE>(vj.w);
+        const unsigned long long k = atomicAdd(rec.count, 1ull);
+        if ((long long)k < rec.cap) {
+            const uint2 wd = pair_words(idi, idj, ks);
+            rec.quad[k] = make_uint4(min(idi, idj), max(idi, idj), wd.x, wd.y);
         }
     }
 }
@@ -280,9 +307,21 @@ __device__ __forceinline__ void pair_checks(const PairP &pp, const FixP &fx, flo
 // warp's owner table (woex/wsi/wrow at stride FT_WSTRIDE).
 struct PairCursor {
     int t, t1, o, enext, si, lrow;
-    float4 pi, vi;
+    float px, py, pz;
+    float4 vi;
     int fx, fy, fz;
 };
+
+__device__ __forceinline__ void cursor_load(PairCursor &c, const ForceTileSmem &S)
+{
+    c.si = S.wsi[c.o];
+    c.lrow = S.wrow[c.o];
+    c.enext = S.woex[c.o + 1];
+    c.px = S.sx[c.si];
+    c.py = S.sy[c.si];
+    c.pz = S.sz[c.si];
+    c.vi = S.sv[c.si];
+}
 
 __device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &S, int t0, int t1, int base, int nown)
 {
@@ -294,11 +333,7 @@ __device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &
     for (int step = 16; step > 0; step >>= 1)
         if (o + step < nown && S.woex[base + o + step] <= t0) o += step;
     c.o = base + o;
-    c.enext = S.woex[c.o + 1];
-    c.si = S.wsi[c.o];
-    c.lrow = S.wrow[c.o];
-    c.pi = ldp(S, c.si);
-    c.vi = S.sv[c.si];
+    cursor_load(c, S);
 }
 
 __device__ __forceinline__ void cursor_flush(PairCursor &c, ForceTileSmem &S)
@@ -317,11 +352,7 @@ __device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
     if (c.t >= c.enext) { // next owner (never empty)
         cursor_flush(c, S);
         ++c.o;
-        c.enext = S.woex[c.o + 1];
-        c.si = S.wsi[c.o];
-        c.lrow = S.wrow[c.o];
-        c.pi = ldp(S, c.si);
-        c.vi = S.sv[c.si];
+        cursor_load(c, S);
     }
     return S.lst[c.lrow + c.t];
 }
@@ -514,9 +545,9 @@ __global__ void __launch_bounds__(FT_NTHR, 3)
         const int c0 = sxa * row;
         const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
-        if (wrap_lo) stage_fix(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
-        stage_fix(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
-        if (wrap_hi) stage_fix(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
+        if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
+        stage_fix<KMODE>(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
+        if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
     }
     __syncthreads();
 
@@ -582,12 +613,12 @@ __global__ void __launch_bounds__(FT_NTHR, 3)
                     a = e;
                 }
                 if (full) {
-                    const float4 pi = ldp(S, s_i), vi = S.sv[s_i];
+                    const float4 pi = ldp<KMODE>(S, s_i), vi = ldv<KMODE>(S, s_i);
                     for (; a < b; ++a) {
                         if (!(r2_one(S, a, px, py, pz) < pp.rc2)) continue;
                         float dx, dy, dz;
                         const float s =
-                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp(S, a), S.sv[a], ks, rec, err, dx, dy, dz);
+                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, a), ldv<KMODE>(S, a), ks, rec, err, dx, dy, dz);
                         const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
                                   qz = to_fixed(s * dz, fx.scale);
                         atomicAdd(&S.acc[0][s_i], qx);
@@ -628,20 +659,27 @@ __global__ void __launch_bounds__(FT_NTHR, 3)
             PairCursor A, B;
             cursor_init(A, S, t0, tm, wb, nown);
             cursor_init(B, S, tm, t1, wb, nown);
+            float amax = 0.0f;
             while (A.t < A.t1) { // B is never longer than A
                 const int ja = cursor_next(A, S);
                 const bool bact = B.t < B.t1;
-                const int jb = bact ? cursor_next(B, S) : B.si; // inactive: self pair, r2 = 0 -> f = 0
+                const int jb = bact ? cursor_next(B, S) : B.si; // idle: self pair, r2 = 0 -> f = 0
+                const float4 vja = S.sv[ja], vjb = S.sv[jb];
                 float dxa, dya, dza, dxb, dyb, dzb;
-                const float sa = pair_core<KMODE>(pp, A.pi, A.vi, ldp(S, ja), S.sv[ja], ks, dxa, dya, dza);
-                const float sb = pair_core<KMODE>(pp, B.pi, B.vi, ldp(S, jb), S.sv[jb], ks, dxb, dyb, dzb);
-                pair_checks<RECORD>(pp, fx, A.pi, ldp(S, ja), sa, dxa, dya, dza, ks, rec, err);
-                if (bact) pair_checks<RECORD>(pp, fx, B.pi, ldp(S, jb), sb, dxb, dyb, dzb, ks, rec, err);
+                const float sa = pair_core<KMODE>(pp, A.px, A.py, A.pz, A.vi, S.sx[ja], S.sy[ja], S.sz[ja], vja, ks,
+                                                  dxa, dya, dza, amax);
+                const float sb = pair_core<KMODE>(pp, B.px, B.py, B.pz, B.vi, S.sx[jb], S.sy[jb], S.sz[jb], vjb, ks,
+                                                  dxb, dyb, dzb, amax);
+                if constexpr (RECORD) {
+                    pair_record<KMODE>(A.vi, vja, dxa, dya, dza, ks, rec);
+                    if (bact) pair_record<KMODE>(B.vi, vjb, dxb, dyb, dzb, ks, rec);
+                }
                 cursor_accumulate(A, S, ja, sa, dxa, dya, dza, fx.scale);
-                if (bact) cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale);
+                cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale); // idle: adds zeros
             }
             cursor_flush(A, S);
             cursor_flush(B, S);
+            if (amax > fx.mag_lim) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(A.vi.w));
         }
         __syncwarp(); // the lists and the owner table are rewritten by the next round
     }

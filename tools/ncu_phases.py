@@ -48,15 +48,19 @@ for r in rows:
     c["inst"] += num(r[hdr["Instructions Executed"]])
     c["tinst"] += num(r[hdr["Thread Instructions Executed"]])
     c["samp"] += num(r[hdr["Warp Stall Sampling (All Samples)"]])
+    c["wf"] += num(r[hdr["L1 Wavefronts Shared"]])
+    c["wfi"] += num(r[hdr["L1 Wavefronts Shared Ideal"]])
     for k, i in hdr.items():
         if k.startswith("stall_") and "Not Issued" not in k:
             c[k] += num(r[i])
 ti = sum(c["inst"] for c in agg.values())
 ts = sum(c["samp"] for c in agg.values())
-print(f"total warp-instr {ti:,}  samples {ts:,}")
+tw = sum(c["wf"] for c in agg.values())
+print(f"total warp-instr {ti:,}  samples {ts:,}  smem wavefronts {tw:,}")
 for lab, c in sorted(agg.items(), key=lambda kv: -kv[1]["inst"]):
     st = sorted(((v, k[6:]) for k, v in c.items() if k.startswith("stall_")), reverse=True)[:4]
     eff = c["tinst"] / max(1, c["inst"]) / 32
     print(f"{lab:24s} instr {100*c['inst']/ti:5.1f}%  lanes {100*eff:4.0f}%  samples {100*c['samp']/max(1,ts):5.1f}%  "
-          f"samp/instr(norm) {c['samp']/max(1,ts)/(c['inst']/ti+1e-12):4.2f}  " +
+          f"samp/instr(norm) {c['samp']/max(1,ts)/(c['inst']/ti+1e-12):4.2f}  "
+          f"smem-wf {100*c['wf']/max(1,tw):4.1f}% (ideal {100*c['wfi']/max(1,tw):4.1f}%)  " +
           " ".join(f"{k}:{100*v/max(1,c['samp']):.0f}%" for v, k in st))
