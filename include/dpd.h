@@ -43,7 +43,8 @@ enum {
     DPD_ERR_CUDA = 3,     /* CUDA runtime error (message in dpd_last_error)               */
     DPD_ERR_NUMERIC = 4,  /* non-finite position/velocity/force (input or during a step)  */
     DPD_ERR_CAPACITY = 5, /* a device buffer (cell, ghost, migration) overflowed          */
-    DPD_ERR_COMM = 6      /* NCCL error (multi-GPU)                                       */
+    DPD_ERR_COMM = 6,     /* NCCL error (multi-GPU)                                       */
+    DPD_ERR_IO = 7        /* file I/O error of the asynchronous writer (dumps, dpd_ioq)   */
 };
 
 /* Create a single-GPU context on the current CUDA device for a periodic box.
@@ -80,6 +81,8 @@ int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
  *   "message_capacity_percent" (distributed contexts) scales the per-direction message
  *                  capacities (default 100; >= 10).
  *   "body_force_mode" 0 = periodic Poiseuille (default), 1 = uniform +f along z.
+ *   "dump_delay_us" (after dpd_dump_open) sleep this long before each snapshot write: a
+ *                  simulated slow disk for overlap tests (default 0).
  *   "row_pruning"  1 = prune stencil rows / end cells farther than r_c (default), 0 = off.
  * Out-of-range values -> DPD_ERR_ARG; unknown names -> DPD_ERR_ARG. */
 int dpd_set_option(dpd_ctx *ctx, const char *name, int64_t value);
@@ -276,6 +279,69 @@ int dpd_debug_philox(int64_t n, const uint32_t *ctr, const uint32_t *key, uint32
 /* Device pair words and Box-Muller xi for n (ida, idb, step lo, step hi) quads under seed:
  * words n x 2 (w0, w1), xi n floats.  Host pointers. */
 int dpd_debug_pair_words(int64_t n, const uint32_t *quad_in, uint64_t seed, uint32_t *words, float *xi);
+
+/* ---- NEXT-4: compute / I/O overlap and the task-scheduled step -----------
+ * PAPER.md §3.4: a "compute task" time-steps on the GPU while a "postprocess
+ * task" does all heavy I/O; a "GPU-aware task scheduler based on the Kahn's
+ * topological sorting algorithm, that supports task execution on concurrent CUDA streams"
+ * orders the ~30 fine-grained tasks of a step.  Here the postprocess task is a
+ * host worker thread per context behind a bounded queue, fed by
+ * device-to-host copies on a separate copy stream into pinned slots.
+ *
+ * dpd_dump_open: start the writer.  path_prefix: files are written as
+ *   <path_prefix>_r<rank>_s<step, 10 digits>.dpd ; queue_depth in [0, 64] (default of the
+ *   Python binding 4): at most that many snapshots wait for the disk; a full queue blocks the
+ *   submitting call (never drops); 0 = synchronous (each dump is written before the call
+ *   returns).  Errors: DPD_ERR_ARG (already open, bad depth), DPD_ERR_CUDA.
+ * dpd_dump_every: inside dpd_step / dpd_step_async, snapshot after every `every`-th step
+ *   (global step index divisible by every; 0 = off).  The snapshot kernel runs on the compute
+ *   stream after the step's forces; the copy-out on the copy stream; the next steps proceed
+ *   without waiting for either.
+ * dpd_dump_now: snapshot of the current state (same path).
+ * dpd_dump_close: drain every pending snapshot, join the writer, free the slots; *written
+ *   (may be NULL) receives the number of snapshots written.  A failed write surfaces as
+ *   DPD_ERR_IO at the next dump submission or here.
+ * File layout (little endian): char magic[8] = "DPDSNAP1"; int64 n, step, rank;
+ *   float64 box[3] (global), origin[3] (this rank's subdomain corner); float32 pos[n][3]
+ *   (global frame); float32 vel[n][3] (full-step velocity, C-6); int32 id[n].  Particles are
+ *   in the rank's cell order (sort by id to compare with dpd_get_particles). */
+int dpd_dump_open(dpd_ctx *ctx, const char *path_prefix, int queue_depth);
+int dpd_dump_every(dpd_ctx *ctx, int64_t every);
+int dpd_dump_now(dpd_ctx *ctx);
+int dpd_dump_close(dpd_ctx *ctx, int64_t *written);
+
+/* The step pipeline as scheduled: one line per task in issue (Kahn) order,
+ *   "<stream slot> <task name>[ <- <predecessor>,...]\n"
+ * slot 0 = compute stream, 1 = communication stream, 2 = copy stream.  with_dump selects
+ * the variant with the snapshot tasks.  buf receives a NUL-terminated string of at most
+ * cap bytes (DPD_ERR_ARG if too small). */
+int dpd_step_schedule(dpd_ctx *ctx, int with_dump, char *buf, int64_t cap);
+
+/* Host-side task graph (the scheduler of dpd_step_schedule, exposed for inspection and
+ * tests; no device work): named tasks on stream slots, edges before -> after, Kahn order.
+ * dpd_tg_order: DPD_ERR_CONFIG (and *n = 0) if the edges contain a cycle; among ready tasks
+ * the earliest added is emitted first.  dpd_tg_edge: DPD_ERR_ARG on unknown ids / self
+ * edges. */
+typedef struct dpd_taskgraph dpd_taskgraph;
+int dpd_tg_create(dpd_taskgraph **out);
+int dpd_tg_add(dpd_taskgraph *g, const char *name, int stream_slot, int32_t *id);
+int dpd_tg_edge(dpd_taskgraph *g, int32_t before, int32_t after);
+int dpd_tg_order(dpd_taskgraph *g, int64_t cap, int32_t *order, int64_t *n);
+void dpd_tg_destroy(dpd_taskgraph *g);
+
+/* Host-side bounded I/O queue (the writer behind the dumps; no GPU needed).  depth as in
+ * dpd_dump_open.  dpd_ioq_write copies `bytes` from data and writes them to path on the
+ * worker after delay_us microseconds (a simulated slow disk for tests; 0 normally); it
+ * blocks while depth writes are pending and returns DPD_ERR_IO (message in
+ * dpd_ioq_last_error) if an EARLIER write failed.  dpd_ioq_close drains every pending write,
+ * joins the worker, frees the queue, stores the number of completed writes and returns
+ * DPD_ERR_IO if a write failed and was not yet reported. */
+typedef struct dpd_ioq dpd_ioq;
+int dpd_ioq_create(int depth, dpd_ioq **out);
+int dpd_ioq_write(dpd_ioq *q, const char *path, const void *data, int64_t bytes, int64_t delay_us);
+int dpd_ioq_pending(dpd_ioq *q, int64_t *n);
+int dpd_ioq_close(dpd_ioq *q, int64_t *completed);
+const char *dpd_ioq_last_error(const dpd_ioq *q);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,7 @@ def _nccl_dirs():
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                  + glob.glob(os.path.join(CSRC, "*.h"))
                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 

@@ -14,9 +14,10 @@ import numpy as np
 
 from . import build as _build
 
-DPD_OK, DPD_ERR_ARG, DPD_ERR_CONFIG, DPD_ERR_CUDA, DPD_ERR_NUMERIC, DPD_ERR_CAPACITY, DPD_ERR_COMM = range(7)
+DPD_OK, DPD_ERR_ARG, DPD_ERR_CONFIG, DPD_ERR_CUDA, DPD_ERR_NUMERIC, DPD_ERR_CAPACITY, DPD_ERR_COMM, \
+    DPD_ERR_IO = range(8)
 _ERR_NAMES = {1: "DPD_ERR_ARG", 2: "DPD_ERR_CONFIG", 3: "DPD_ERR_CUDA", 4: "DPD_ERR_NUMERIC",
-              5: "DPD_ERR_CAPACITY", 6: "DPD_ERR_COMM"}
+              5: "DPD_ERR_CAPACITY", 6: "DPD_ERR_COMM", 7: "DPD_ERR_IO"}
 
 
 class DPDError(RuntimeError):
@@ -75,6 +76,21 @@ SIGNATURES = [
     ("dpd_get_species_ex", C.c_int, [_vp, C.c_int64, _vp, _vp, _P(C.c_int64)]),
     ("dpd_debug_philox", C.c_int, [C.c_int64, _vp, _vp, _vp]),
     ("dpd_debug_pair_words", C.c_int, [C.c_int64, _vp, C.c_uint64, _vp, _vp]),
+    ("dpd_dump_open", C.c_int, [_vp, C.c_char_p, C.c_int]),
+    ("dpd_dump_every", C.c_int, [_vp, C.c_int64]),
+    ("dpd_dump_now", C.c_int, [_vp]),
+    ("dpd_dump_close", C.c_int, [_vp, _P(C.c_int64)]),
+    ("dpd_step_schedule", C.c_int, [_vp, C.c_int, C.c_char_p, C.c_int64]),
+    ("dpd_tg_create", C.c_int, [_P(_vp)]),
+    ("dpd_tg_add", C.c_int, [_vp, C.c_char_p, C.c_int, _P(C.c_int32)]),
+    ("dpd_tg_edge", C.c_int, [_vp, C.c_int32, C.c_int32]),
+    ("dpd_tg_order", C.c_int, [_vp, C.c_int64, _vp, _P(C.c_int64)]),
+    ("dpd_tg_destroy", None, [_vp]),
+    ("dpd_ioq_create", C.c_int, [C.c_int, _P(_vp)]),
+    ("dpd_ioq_write", C.c_int, [_vp, C.c_char_p, _vp, C.c_int64, C.c_int64]),
+    ("dpd_ioq_pending", C.c_int, [_vp, _P(C.c_int64)]),
+    ("dpd_ioq_close", C.c_int, [_vp, _P(C.c_int64)]),
+    ("dpd_ioq_last_error", C.c_char_p, [_vp]),
 ]
 
 
@@ -326,6 +342,128 @@ def dpd_debug_pair_words(quads, seed):
     if code != DPD_OK:
         raise DPDError(code, "dpd_debug_pair_words")
     return words, xi
+
+
+# ---- NEXT-4: asynchronous dumps, the step schedule, task graph and I/O queue ----------------
+def dpd_dump_open(ctx, path_prefix, queue_depth=4):
+    _check(ctx, load().dpd_dump_open(ctx, os.fsencode(path_prefix), int(queue_depth)))
+
+
+def dpd_dump_every(ctx, every):
+    _check(ctx, load().dpd_dump_every(ctx, int(every)))
+
+
+def dpd_dump_now(ctx):
+    _check(ctx, load().dpd_dump_now(ctx))
+
+
+def dpd_dump_close(ctx):
+    """Drain and join the writer; returns the number of snapshots written."""
+    n = C.c_int64()
+    _check(ctx, load().dpd_dump_close(ctx, C.byref(n)))
+    return n.value
+
+
+def dpd_step_schedule(ctx, with_dump=False):
+    """[(stream slot, task name, [predecessors])] in issue order."""
+    buf = C.create_string_buffer(8192)
+    _check(ctx, load().dpd_step_schedule(ctx, int(bool(with_dump)), buf, len(buf)))
+    out = []
+    for line in buf.value.decode().splitlines():
+        head, _, preds = line.partition(" <- ")
+        slot, name = head.split(" ", 1)
+        out.append((int(slot), name, preds.split(",") if preds else []))
+    return out
+
+
+def read_dump(path):
+    """Read one snapshot file (layout in include/dpd.h) -> dict of numpy arrays."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:8] != b"DPDSNAP1":
+        raise ValueError(f"{path}: not a DPD snapshot")
+    n, step, rank = np.frombuffer(raw, np.int64, 3, 8)
+    box = np.frombuffer(raw, np.float64, 3, 32)
+    origin = np.frombuffer(raw, np.float64, 3, 56)
+    o = 80
+    pos = np.frombuffer(raw, np.float32, 3 * n, o).reshape(n, 3)
+    vel = np.frombuffer(raw, np.float32, 3 * n, o + 12 * n).reshape(n, 3)
+    ids = np.frombuffer(raw, np.int32, n, o + 24 * n)
+    return {"n": int(n), "step": int(step), "rank": int(rank), "box": box.copy(), "origin": origin.copy(),
+            "pos": pos.copy(), "vel": vel.copy(), "ids": ids.copy()}
+
+
+class TaskGraph:
+    """Host-side Kahn scheduler of the step (dpd_tg_*): add(name, slot) -> id, edge(a, b), order()."""
+
+    def __init__(self):
+        self.h = C.c_void_p()
+        code = load().dpd_tg_create(C.byref(self.h))
+        if code != DPD_OK:
+            raise DPDError(code, "dpd_tg_create")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            load().dpd_tg_destroy(self.h)
+            self.h = None
+
+    def add(self, name, slot=0):
+        i = C.c_int32()
+        code = load().dpd_tg_add(self.h, name.encode(), int(slot), C.byref(i))
+        if code != DPD_OK:
+            raise DPDError(code, "dpd_tg_add")
+        return i.value
+
+    def edge(self, before, after):
+        code = load().dpd_tg_edge(self.h, int(before), int(after))
+        if code != DPD_OK:
+            raise DPDError(code, "dpd_tg_edge")
+
+    def order(self):
+        n = C.c_int64()
+        buf = np.empty(4096, np.int32)
+        code = load().dpd_tg_order(self.h, len(buf), _ptr(buf), C.byref(n))
+        if code != DPD_OK:
+            raise DPDError(code, "dpd_tg_order: cycle" if code == DPD_ERR_CONFIG else "dpd_tg_order")
+        return buf[: n.value].tolist()
+
+
+class IoQueue:
+    """Host-side bounded writer (dpd_ioq_*): write(path, bytes, delay_us) / pending() / close()."""
+
+    def __init__(self, depth=4):
+        self.h = C.c_void_p()
+        code = load().dpd_ioq_create(int(depth), C.byref(self.h))
+        if code != DPD_OK:
+            raise DPDError(code, "dpd_ioq_create")
+
+    def write(self, path, data, delay_us=0):
+        buf = np.frombuffer(bytes(data), np.uint8)
+        code = load().dpd_ioq_write(self.h, os.fsencode(path), _ptr(buf) if len(buf) else None, len(buf),
+                                    int(delay_us))
+        if code != DPD_OK:
+            raise DPDError(code, load().dpd_ioq_last_error(self.h).decode())
+
+    def pending(self):
+        n = C.c_int64()
+        load().dpd_ioq_pending(self.h, C.byref(n))
+        return n.value
+
+    def close(self):
+        """Drain, join, free; returns the number of completed writes."""
+        n = C.c_int64()
+        h, self.h = self.h, None
+        code = load().dpd_ioq_close(h, C.byref(n))
+        if code != DPD_OK:
+            raise DPDError(code, "a queued write failed")
+        return n.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                self.close()
+            except Exception:
+                pass
 
 
 class DPD:

@@ -23,6 +23,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -35,6 +39,7 @@
 #include "dpd_force_cells.cuh"
 #include "dpd_force_tile.cuh"
 #include "dpd_kernels.cuh"
+#include "dpd_sched.h"
 
 using namespace dpd;
 
@@ -103,6 +108,31 @@ struct MsgArea {
 
 } // namespace
 
+// Asynchronous snapshot dumps (NEXT-4): one device staging block, `depth + 1` pinned host
+// slots and the I/O worker (IoQueue) writing <prefix>_r<rank>_s<step>.dpd files.
+struct DumpSlot {
+    char *host = nullptr;
+    cudaEvent_t copied = nullptr;
+    bool busy = false;
+};
+
+struct DumpState {
+    std::string prefix;
+    int depth = 4;
+    int device = 0;
+    int64_t every = 0;
+    int64_t cap = 0;           // particles per staging block / slot
+    int64_t delay_us = 0;      // simulated slow disk (tests)
+    char *dev = nullptr;       // device staging block
+    cudaEvent_t staged_free = nullptr; // last D2H of the staging block finished
+    std::vector<DumpSlot> slots;
+    std::mutex m;
+    std::condition_variable cv;
+    dpd::IoQueue *q = nullptr;
+    int64_t submitted = 0;
+    int last_slot = -1;
+};
+
 struct dpd_ctx {
     // parameters
     double box[3];   // global box
@@ -168,6 +198,11 @@ struct dpd_ctx {
     int64_t launches = 0;
     int64_t fallback[3] = {0, 0, 0}; // tiled kernel: staged / home capacity tiles, full-list particles
     std::string last_error;
+    // NEXT-4: the step as a task graph and asynchronous dumps
+    dpd::TaskGraph *step_graph[2] = {nullptr, nullptr}; // [0] plain step, [1] step + snapshot
+    IntegP ip_step{};
+    cudaStream_t copy_stream = nullptr;
+    DumpState *dump = nullptr;
 };
 
 namespace {
@@ -626,27 +661,209 @@ int setup_messages(dpd_ctx *c, double rho)
     return DPD_OK;
 }
 
-// ---- one step of one context (NCCL or single) -------------------------------------------
-int step_one(dpd_ctx *c)
+// ---- asynchronous snapshot (NEXT-4) ------------------------------------------------------
+size_t dump_bytes(int64_t cap) { return 16 + (size_t)cap * 28; }
+
+// Snapshot of the current state into the device staging block (on the compute stream, after
+// the previous copy-out of that block).
+int dump_snapshot(dpd_ctx *c, cudaStream_t st)
 {
-    const float kick = c->primed ? (float)(0.5 * c->dt) : (float)c->dt;
-    const IntegP ip = integ(c, (float)c->dt, kick);
-    TRY(phase_bin(c, ip));
-    if (c->dist) TRY(exchange_nccl(c, c->mig, c->stream));
-    TRY(phase_sort(c, ip));
-    c->step += 1;
-    if (c->dist) {
-        TRY(phase_ghost_pack(c));
-        CUDA_TRY(c, cudaEventRecord(c->ev_pack, c->stream));
-        CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0));
-        TRY(exchange_nccl(c, c->gh, c->comm_stream));
-        CUDA_TRY(c, cudaEventRecord(c->ev_ghost, c->comm_stream));
+    DumpState *d = c->dump;
+    if (c->n_cap > d->cap) {
+        // a larger state: wait for the writer to finish with every slot, then re-allocate
+        {
+            std::unique_lock<std::mutex> lk(d->m);
+            d->cv.wait(lk, [d] {
+                for (auto &sl : d->slots)
+                    if (sl.busy) return false;
+                return true;
+            });
+        }
+        CUDA_TRY(c, cudaStreamSynchronize(c->copy_stream));
+        if (d->dev) cudaFree(d->dev);
+        d->dev = nullptr;
+        for (auto &sl : d->slots) {
+            if (sl.host) cudaFreeHost(sl.host);
+            sl.host = nullptr;
+        }
+        d->cap = c->n_cap;
+        CUDA_TRY(c, cudaMalloc(&d->dev, dump_bytes(d->cap)));
+        for (auto &sl : d->slots) CUDA_TRY(c, cudaMallocHost(&sl.host, dump_bytes(d->cap)));
     }
-    TRY(force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false));
-    if (c->dist) {
-        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_ghost, 0));
-        TRY(phase_halo(c, c->step));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, d->staged_free, 0));
+    const int b = c->cur;
+    const float hk = c->primed ? 0.0f : (float)(0.5 * c->dt);
+    const IntegP ip = integ(c, 0.0f, 0.0f);
+    const float3 org = make_float3(c->origin[0], c->origin[1], c->origin[2]);
+    const int64_t cap = d->cap;
+    long long *hdr = reinterpret_cast<long long *>(d->dev);
+    float *p3 = reinterpret_cast<float *>(d->dev + 16);
+    float *v3 = p3 + 3 * cap;
+    int32_t *ids = reinterpret_cast<int32_t *>(v3 + 3 * cap);
+    const int nb = (int)std::min<int64_t>(nblk(std::max<int64_t>(cap, 1), 256), 148 * 8);
+    return launch(c, KID_GATHER, [&] {
+        k_snapshot<<<nb, 256, 0, st>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), (int)cap, hk, ip, org, hdr,
+                                       p3, v3, ids);
+    });
+}
+
+// Copy-out of the staging block into a free pinned slot (copy stream) and hand-off to the
+// I/O worker, which waits for the copy and writes the file.  Blocks only when every slot is
+// still owned by the writer (backpressure, nothing dropped).
+int dump_copyout(dpd_ctx *c, cudaStream_t st)
+{
+    DumpState *d = c->dump;
+    int k = -1;
+    {
+        std::unique_lock<std::mutex> lk(d->m);
+        d->cv.wait(lk, [d, &k] {
+            for (int i = 0; i < (int)d->slots.size(); ++i) {
+                const int j = (d->last_slot + 1 + i) % (int)d->slots.size();
+                if (!d->slots[j].busy) {
+                    k = j;
+                    return true;
+                }
+            }
+            return false;
+        });
+        d->slots[k].busy = true;
+        d->last_slot = k;
     }
+    DumpSlot &sl = d->slots[k];
+    CUDA_TRY(c, cudaMemcpyAsync(sl.host, d->dev, dump_bytes(d->cap), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(c, cudaEventRecord(sl.copied, st));
+    CUDA_TRY(c, cudaEventRecord(d->staged_free, st));
+    char path[4096];
+    snprintf(path, sizeof path, "%s_r%d_s%010lld.dpd", d->prefix.c_str(), c->rank, (long long)c->step);
+    const std::string fpath = path;
+    const int64_t step = c->step, cap = d->cap;
+    const int rank = c->rank;
+    double box[3], org[3];
+    for (int q = 0; q < 3; ++q) {
+        box[q] = c->box[q];
+        org[q] = c->origin[q];
+    }
+    auto job = [d, k, fpath, step, cap, rank, box, org](std::string &err) -> int {
+        DumpSlot &s2 = d->slots[k];
+        int rc = 0;
+        cudaSetDevice(d->device);
+        if (cudaEventSynchronize(s2.copied) != cudaSuccess) {
+            err = "snapshot copy failed";
+            rc = -1;
+        }
+        if (rc == 0 && d->delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(d->delay_us));
+        if (rc == 0) {
+            const long long n = *reinterpret_cast<const long long *>(s2.host);
+            FILE *f = fopen(fpath.c_str(), "wb");
+            if (!f) {
+                err = "cannot open " + fpath;
+                rc = -1;
+            } else {
+                // header: magic, n, step, rank, box[3], origin of the subdomain[3]
+                const char magic[8] = {'D', 'P', 'D', 'S', 'N', 'A', 'P', '1'};
+                const int64_t hdr[3] = {(int64_t)n, step, (int64_t)rank};
+                const char *p3 = s2.host + 16;
+                const char *v3 = p3 + 12 * cap;
+                const char *id = v3 + 12 * cap;
+                bool ok = fwrite(magic, 1, 8, f) == 8 && fwrite(hdr, 8, 3, f) == 3 && fwrite(box, 8, 3, f) == 3 &&
+                          fwrite(org, 8, 3, f) == 3;
+                ok = ok && fwrite(p3, 12, (size_t)n, f) == (size_t)n && fwrite(v3, 12, (size_t)n, f) == (size_t)n &&
+                     fwrite(id, 4, (size_t)n, f) == (size_t)n;
+                ok = (fclose(f) == 0) && ok;
+                if (!ok) {
+                    err = "short write to " + fpath;
+                    rc = -1;
+                }
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(d->m);
+            s2.busy = false;
+        }
+        d->cv.notify_all();
+        return rc;
+    };
+    std::string err;
+    if (d->q->submit(job, err) != 0) return fail(c, DPD_ERR_IO, "dump: %s", err.c_str());
+    ++d->submitted;
+    return DPD_OK;
+}
+
+// ---- one step of one context as a task graph (NCCL or single) ----------------------------
+// Tasks (stream slot): kick_drift_bin (0) -> [migrate_exchange (0)] -> scan_scatter (0) ->
+// [ghost_pack (0) -> ghost_exchange (1, comm stream)] ; force_local (0) -> [halo_force (0),
+// after ghost_exchange] -> [snapshot (0) -> snapshot_d2h (2, copy stream)].  Kahn's order
+// issues ghost_exchange before force_local, so the exchange overlaps the interior forces
+// (P:244-247); cross-stream edges become CUDA events.
+dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
+{
+    auto *g = new dpd::TaskGraph();
+    const int t_bin = g->add("kick_drift_bin", 0, [c](cudaStream_t) {
+        const float kick = c->primed ? (float)(0.5 * c->dt) : (float)c->dt;
+        c->ip_step = integ(c, (float)c->dt, kick);
+        return phase_bin(c, c->ip_step);
+    });
+    int last = t_bin;
+    if (c->dist) {
+        const int t = g->add("migrate_exchange", 0, [c](cudaStream_t s) { return exchange_nccl(c, c->mig, s); });
+        g->edge(last, t);
+        last = t;
+    }
+    const int t_sort = g->add("scan_scatter", 0, [c](cudaStream_t) -> int {
+        TRY(phase_sort(c, c->ip_step));
+        c->step += 1;
+        return DPD_OK;
+    });
+    g->edge(last, t_sort);
+    int t_gx = -1;
+    if (c->dist) {
+        const int t_gp = g->add("ghost_pack", 0, [c](cudaStream_t) { return phase_ghost_pack(c); });
+        g->edge(t_sort, t_gp);
+        t_gx = g->add("ghost_exchange", 1, [c](cudaStream_t s) { return exchange_nccl(c, c->gh, s); });
+        g->edge(t_gp, t_gx);
+    }
+    const int t_force = g->add("force_local", 0, [c](cudaStream_t) {
+        return force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false);
+    });
+    g->edge(t_sort, t_force);
+    last = t_force;
+    if (c->dist) {
+        const int t_h = g->add("halo_force", 0, [c](cudaStream_t) { return phase_halo(c, c->step); });
+        g->edge(t_force, t_h);
+        g->edge(t_gx, t_h);
+        last = t_h;
+    }
+    if (with_dump) {
+        const int t_s = g->add("snapshot", 0, [c](cudaStream_t s) { return dump_snapshot(c, s); });
+        g->edge(last, t_s);
+        const int t_c = g->add("snapshot_d2h", 2, [c](cudaStream_t s) { return dump_copyout(c, s); });
+        g->edge(t_s, t_c);
+    }
+    if (g->build() != 0) {
+        delete g;
+        return nullptr;
+    }
+    return g;
+}
+
+int run_graph(dpd_ctx *c, dpd::TaskGraph *g)
+{
+    const cudaStream_t streams[3] = {c->stream, c->comm_stream ? c->comm_stream : c->stream,
+                                     c->copy_stream ? c->copy_stream : c->stream};
+    const int rc = g->run(streams);
+    if (rc == -1) return fail(c, DPD_ERR_CONFIG, "step task graph has a cycle");
+    if (rc == -2) return fail(c, DPD_ERR_CUDA, "task graph: %s", cudaGetErrorString(cudaGetLastError()));
+    return rc;
+}
+
+int step_one(dpd_ctx *c, bool with_dump = false)
+{
+    const int k = with_dump ? 1 : 0;
+    if (!c->step_graph[k]) {
+        c->step_graph[k] = build_step_graph(c, with_dump);
+        if (!c->step_graph[k]) return fail(c, DPD_ERR_CONFIG, "step task graph has a cycle");
+    }
+    TRY(run_graph(c, c->step_graph[k]));
     c->primed = false;
     return DPD_OK;
 }
@@ -928,6 +1145,8 @@ void dpd_destroy(dpd_ctx *c)
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    if (c->dump) dpd_dump_close(c, nullptr);
+    for (auto *g : c->step_graph) delete g;
     for (int b = 0; b < 2; ++b) {
         c->pos[b].release();
         c->vel[b].release();
@@ -1014,6 +1233,12 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
     if (strcmp(name, "row_pruning") == 0) {
         if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "row_pruning must be 0 or 1");
         c->fix.prune = (int)value;
+        return DPD_OK;
+    }
+    if (strcmp(name, "dump_delay_us") == 0) {
+        if (!c->dump) return fail(c, DPD_ERR_ARG, "dpd_dump_open first");
+        if (value < 0 || value > 60000000) return fail(c, DPD_ERR_ARG, "dump_delay_us out of range");
+        c->dump->delay_us = value;
         return DPD_OK;
     }
     if (strcmp(name, "message_capacity_percent") == 0) {
@@ -1325,7 +1550,10 @@ int dpd_step_async(dpd_ctx *c, int64_t nsteps)
     if (!c) return DPD_ERR_ARG;
     if (nsteps < 0) return fail(c, DPD_ERR_ARG, "nsteps must be >= 0");
     if (c->group) return fail(c, DPD_ERR_ARG, "group members are stepped with dpd_group_step");
-    for (int64_t it = 0; it < nsteps; ++it) TRY(step_one(c));
+    for (int64_t it = 0; it < nsteps; ++it) {
+        const bool due = c->dump && c->dump->every > 0 && (c->step + 1) % c->dump->every == 0;
+        TRY(step_one(c, due));
+    }
     return DPD_OK;
 }
 
@@ -1741,4 +1969,190 @@ int dpd_get_forces_ex(dpd_ctx *c, int64_t cap, float *f, int32_t *ids, int64_t *
     return copy_ids(c, ids);
 }
 
+// ---- NEXT-4: asynchronous dumps, step schedule, task graph and I/O queue (host) ----------
+int dpd_dump_open(dpd_ctx *c, const char *path_prefix, int queue_depth)
+{
+    if (!c || !path_prefix) return DPD_ERR_ARG;
+    if (queue_depth < 0 || queue_depth > 64) return fail(c, DPD_ERR_ARG, "queue_depth must be in [0, 64]");
+    if (c->dump) return fail(c, DPD_ERR_ARG, "dumps already open; dpd_dump_close first");
+    auto *d = new DumpState();
+    d->prefix = path_prefix;
+    d->depth = queue_depth;
+    cudaGetDevice(&d->device);
+    d->slots.resize(queue_depth + 1);
+    for (auto &sl : d->slots) CUDA_TRY(c, cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&d->staged_free, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventRecord(d->staged_free, c->stream));
+    if (!c->copy_stream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    d->q = new dpd::IoQueue(queue_depth);
+    c->dump = d;
+    return DPD_OK;
+}
+
+int dpd_dump_every(dpd_ctx *c, int64_t every)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (!c->dump) return fail(c, DPD_ERR_ARG, "dpd_dump_open first");
+    if (every < 0) return fail(c, DPD_ERR_ARG, "every must be >= 0");
+    if (c->group) return fail(c, DPD_ERR_ARG, "dumps are per NCCL / single context");
+    c->dump->every = every;
+    return DPD_OK;
+}
+
+int dpd_dump_now(dpd_ctx *c)
+{
+    if (!c) return DPD_ERR_ARG;
+    if (!c->dump) return fail(c, DPD_ERR_ARG, "dpd_dump_open first");
+    TRY(dump_snapshot(c, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->dump->staged_free, c->stream)); // orders the copy-out after the snapshot
+    CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->dump->staged_free, 0));
+    return dump_copyout(c, c->copy_stream);
+}
+
+int dpd_dump_close(dpd_ctx *c, int64_t *written)
+{
+    if (!c) return DPD_ERR_ARG;
+    DumpState *d = c->dump;
+    if (!d) return fail(c, DPD_ERR_ARG, "dumps are not open");
+    std::string err;
+    const int rc = d->q->close(&err);
+    if (written) *written = d->q->completed();
+    delete d->q;
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    for (auto &sl : d->slots) {
+        if (sl.host) cudaFreeHost(sl.host);
+        if (sl.copied) cudaEventDestroy(sl.copied);
+    }
+    if (d->staged_free) cudaEventDestroy(d->staged_free);
+    if (d->dev) cudaFree(d->dev);
+    delete d;
+    c->dump = nullptr;
+    delete c->step_graph[1]; // the snapshot tasks refer to the closed state
+    c->step_graph[1] = nullptr;
+    if (rc != 0) return fail(c, DPD_ERR_IO, "dump: %s", err.c_str());
+    return DPD_OK;
+}
+
+int dpd_step_schedule(dpd_ctx *c, int with_dump, char *buf, int64_t cap)
+{
+    if (!c || !buf || cap <= 0) return DPD_ERR_ARG;
+    dpd::TaskGraph *g = build_step_graph(c, with_dump != 0);
+    if (!g) return fail(c, DPD_ERR_CONFIG, "step task graph has a cycle");
+    std::string out;
+    for (int u : g->order) {
+        const auto &t = g->tasks[u];
+        out += std::to_string(t.slot) + " " + t.name;
+        for (size_t k = 0; k < t.pred.size(); ++k) out += (k ? "," : " <- ") + g->tasks[t.pred[k]].name;
+        out += "\n";
+    }
+    delete g;
+    if ((int64_t)out.size() + 1 > cap) return fail(c, DPD_ERR_ARG, "buffer too small (%zu bytes needed)", out.size() + 1);
+    memcpy(buf, out.c_str(), out.size() + 1);
+    return DPD_OK;
+}
+
 } // extern "C"
+
+struct dpd_taskgraph {
+    dpd::TaskGraph g;
+};
+
+struct dpd_ioq {
+    dpd::IoQueue *q = nullptr;
+    std::string last_error;
+};
+
+extern "C" {
+
+int dpd_tg_create(dpd_taskgraph **out)
+{
+    if (!out) return DPD_ERR_ARG;
+    *out = new dpd_taskgraph();
+    return DPD_OK;
+}
+
+int dpd_tg_add(dpd_taskgraph *g, const char *name, int slot, int32_t *id)
+{
+    if (!g || !name || !id || slot < 0) return DPD_ERR_ARG;
+    *id = g->g.add(name, slot);
+    return DPD_OK;
+}
+
+int dpd_tg_edge(dpd_taskgraph *g, int32_t before, int32_t after)
+{
+    if (!g) return DPD_ERR_ARG;
+    return g->g.edge(before, after) == 0 ? DPD_OK : DPD_ERR_ARG;
+}
+
+int dpd_tg_order(dpd_taskgraph *g, int64_t cap, int32_t *order, int64_t *n)
+{
+    if (!g || !n) return DPD_ERR_ARG;
+    if (g->g.build() != 0) {
+        *n = 0;
+        return DPD_ERR_CONFIG;
+    }
+    *n = (int64_t)g->g.order.size();
+    if (cap < *n || (*n > 0 && !order)) return DPD_ERR_ARG;
+    for (int64_t k = 0; k < *n; ++k) order[k] = g->g.order[k];
+    return DPD_OK;
+}
+
+void dpd_tg_destroy(dpd_taskgraph *g) { delete g; }
+
+int dpd_ioq_create(int depth, dpd_ioq **out)
+{
+    if (!out || depth < 0 || depth > 64) return DPD_ERR_ARG;
+    *out = new dpd_ioq();
+    (*out)->q = new dpd::IoQueue(depth);
+    return DPD_OK;
+}
+
+int dpd_ioq_write(dpd_ioq *q, const char *path, const void *data, int64_t bytes, int64_t delay_us)
+{
+    if (!q || !path || bytes < 0 || (bytes > 0 && !data) || delay_us < 0) return DPD_ERR_ARG;
+    auto buf = std::make_shared<std::vector<char>>((const char *)data, (const char *)data + bytes);
+    const std::string p = path;
+    auto job = [buf, p, delay_us](std::string &err) -> int {
+        if (delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(delay_us));
+        FILE *f = fopen(p.c_str(), "wb");
+        if (!f) {
+            err = "cannot open " + p;
+            return -1;
+        }
+        const bool ok = fwrite(buf->data(), 1, buf->size(), f) == buf->size();
+        if (fclose(f) != 0 || !ok) {
+            err = "short write to " + p;
+            return -1;
+        }
+        return 0;
+    };
+    std::string err;
+    if (q->q->submit(job, err) != 0) {
+        q->last_error = err;
+        return DPD_ERR_IO;
+    }
+    return DPD_OK;
+}
+
+int dpd_ioq_pending(dpd_ioq *q, int64_t *n)
+{
+    if (!q || !n) return DPD_ERR_ARG;
+    *n = q->q->pending();
+    return DPD_OK;
+}
+
+int dpd_ioq_close(dpd_ioq *q, int64_t *completed)
+{
+    if (!q) return DPD_ERR_ARG;
+    std::string err;
+    const int rc = q->q->close(&err);
+    if (completed) *completed = q->q->completed();
+    delete q->q;
+    delete q;
+    return rc == 0 ? DPD_OK : DPD_ERR_IO;
+}
+
+const char *dpd_ioq_last_error(const dpd_ioq *q) { return q ? q->last_error.c_str() : "null queue"; }
+
+} // extern "C"
+

@@ -563,6 +563,34 @@ __global__ void k_gather_id(const float4 *__restrict__ pos, const float4 *__rest
     }
 }
 
+// Snapshot of the asynchronous dump: the first *count
+// particles (device-resident count) in cell order -- positions in the global frame,
+// full-step velocities (row a6, as k_gather_id) and ids -- into a staging block
+// [int64 count | pad][pos n x 3][vel n x 3][ids n] laid out for `cap` particles.
+__global__ void k_snapshot(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+                           const float4 *__restrict__ frc, const int *__restrict__ count, int cap, float hk,
+                           IntegP ip, float3 origin, long long *__restrict__ hdr, float *__restrict__ pos3,
+                           float *__restrict__ vel3, int32_t *__restrict__ ids)
+{
+    const int n = min(*count, cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        hdr[0] = n;
+        hdr[1] = 0;
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = pos[i], v = vel[i], f = frc[i];
+        pos3[3 * i + 0] = p.x + origin.x;
+        pos3[3 * i + 1] = p.y + origin.y;
+        pos3[3 * i + 2] = p.z + origin.z;
+        const float fb = body_fz(ip, p.x);
+        const float h = (ip.frozen_mask && is_frozen(ip, v)) ? 0.0f : hk;
+        vel3[3 * i + 0] = __fmaf_rn(h, f.x, v.x);
+        vel3[3 * i + 1] = __fmaf_rn(h, f.y, v.y);
+        vel3[3 * i + 2] = __fmaf_rn(h, __fadd_rn(f.z, fb), v.z);
+        ids[i] = __float_as_int(p.w);
+    }
+}
+
 __global__ void k_ids_cells(const float4 *__restrict__ pos, int n, Geom g, int32_t *__restrict__ ids,
                             int32_t *__restrict__ cell_of_id)
 {

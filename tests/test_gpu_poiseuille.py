@@ -48,9 +48,12 @@ def fit_eta(xc, vz, L, rho, f):
 
 def test_periodic_poiseuille_parabola_fig3_parameters():
     # Fig.-3 parameters: rho = 8, a = 10, gamma = 20, kT = 1, k = 0.5, dt = 0.005
+    # f = 0.1 (v_max ~ 0.4, Re ~ 1: linear response) and 600 samples keep the thermal noise
+    # of the 16 bin means well below the 5 % bar (at f = 0.05 / 300 samples the L2 error of
+    # a correct run scattered around 4-6 % with the trajectory)
     cfg = workloads.with_box(workloads.CONFIGS["pois96"], (16.0, 16.0, 16.0))
-    f = 0.05
-    xc, vz = run_profile(cfg, f, warm=4000, nsample=300, every=10, nbins=16)
+    f = 0.1
+    xc, vz = run_profile(cfg, f, warm=4000, nsample=600, every=10, nbins=16)
     eta_lo, eta_hi, l2 = fit_eta(xc, vz, 16.0, 8.0, f)
     # L2 error of the parabola < 5 %, the two half-domain fits agree within 5 %
     assert l2 < 0.05, (l2, vz)
