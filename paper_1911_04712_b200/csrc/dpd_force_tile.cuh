@@ -35,6 +35,13 @@ constexpr int FT_SCAP = 1024;                 // staged particles (mean 864, sd 
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
 constexpr int FT_LCAP = 40;                   // hits per home particle (mean 16.8, sd 4.1)
 constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 21 words per list (odd): conflict-free appends
+#ifndef FT_NCUR_DEF
+#define FT_NCUR_DEF 2
+#endif
+constexpr int FT_NCUR = FT_NCUR_DEF;          // independent pair chains per lane (ILP)
+#ifndef FT_MINB
+#define FT_MINB 3                             // resident tiles per SM (register budget)
+#endif
 constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32 owners + sentinel)
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
@@ -429,7 +436,7 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
 }
 
 template <bool RECORD, int KMODE>
-__global__ void __launch_bounds__(FT_NTHR, 3)
+__global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
                  const int *__restrict__ start, Geom g, PairP pp, FixP fx, uint32_t s_lo, uint32_t s_hi,
                  PairRec rec, int *err)
@@ -655,31 +662,39 @@ __global__ void __launch_bounds__(FT_NTHR, 3)
             const int C = (tot + 31) >> 5;
             const int t0 = min(lane * C, tot);
             const int t1 = min(t0 + C, tot);
-            const int tm = t0 + ((t1 - t0 + 1) >> 1);
-            PairCursor A, B;
-            cursor_init(A, S, t0, tm, wb, nown);
-            cursor_init(B, S, tm, t1, wb, nown);
+            const int q = (t1 - t0 + FT_NCUR - 1) / FT_NCUR;
+            PairCursor cu[FT_NCUR];
+#pragma unroll
+            for (int k = 0; k < FT_NCUR; ++k) cursor_init(cu[k], S, min(t0 + k * q, t1), min(t0 + (k + 1) * q, t1), wb, nown);
             float amax = 0.0f;
-            while (A.t < A.t1) { // B is never longer than A
-                const int ja = cursor_next(A, S);
-                const bool bact = B.t < B.t1;
-                const int jb = bact ? cursor_next(B, S) : B.si; // idle: self pair, r2 = 0 -> f = 0
-                const float4 vja = S.sv[ja], vjb = S.sv[jb];
-                float dxa, dya, dza, dxb, dyb, dzb;
-                const float sa = pair_core<KMODE>(pp, A.px, A.py, A.pz, A.vi, S.sx[ja], S.sy[ja], S.sz[ja], vja, ks,
-                                                  dxa, dya, dza, amax);
-                const float sb = pair_core<KMODE>(pp, B.px, B.py, B.pz, B.vi, S.sx[jb], S.sy[jb], S.sz[jb], vjb, ks,
-                                                  dxb, dyb, dzb, amax);
-                if constexpr (RECORD) {
-                    pair_record<KMODE>(A.vi, vja, dxa, dya, dza, ks, rec);
-                    if (bact) pair_record<KMODE>(B.vi, vjb, dxb, dyb, dzb, ks, rec);
+            while (cu[0].t < cu[0].t1) { // later cursors are never longer than the first
+                int j[FT_NCUR];
+                bool act[FT_NCUR];
+#pragma unroll
+                for (int k = 0; k < FT_NCUR; ++k) {
+                    act[k] = (k == 0) || cu[k].t < cu[k].t1;
+                    j[k] = act[k] ? cursor_next(cu[k], S) : cu[k].si; // idle: self pair, r2 = 0 -> f = 0
                 }
-                cursor_accumulate(A, S, ja, sa, dxa, dya, dza, fx.scale);
-                cursor_accumulate(B, S, jb, sb, dxb, dyb, dzb, fx.scale); // idle: adds zeros
+                float4 vj[FT_NCUR];
+                float sv_[FT_NCUR], dx[FT_NCUR], dy[FT_NCUR], dz[FT_NCUR];
+#pragma unroll
+                for (int k = 0; k < FT_NCUR; ++k) vj[k] = S.sv[j[k]];
+#pragma unroll
+                for (int k = 0; k < FT_NCUR; ++k)
+                    sv_[k] = pair_core<KMODE>(pp, cu[k].px, cu[k].py, cu[k].pz, cu[k].vi, S.sx[j[k]], S.sy[j[k]],
+                                              S.sz[j[k]], vj[k], ks, dx[k], dy[k], dz[k], amax);
+                if constexpr (RECORD) {
+#pragma unroll
+                    for (int k = 0; k < FT_NCUR; ++k)
+                        if (act[k]) pair_record<KMODE>(cu[k].vi, vj[k], dx[k], dy[k], dz[k], ks, rec);
+                }
+#pragma unroll
+                for (int k = 0; k < FT_NCUR; ++k)
+                    cursor_accumulate(cu[k], S, j[k], sv_[k], dx[k], dy[k], dz[k], fx.scale); // idle: adds zeros
             }
-            cursor_flush(A, S);
-            cursor_flush(B, S);
-            if (amax > fx.mag_lim) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(A.vi.w));
+#pragma unroll
+            for (int k = 0; k < FT_NCUR; ++k) cursor_flush(cu[k], S);
+            if (amax > fx.mag_lim) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(cu[0].vi.w));
         }
         __syncwarp(); // the lists and the owner table are rewritten by the next round
     }
