@@ -436,6 +436,19 @@ int phase_ghost_pack(dpd_ctx *c)
 }
 
 // a5: local-local pairs at RNG step index `step`.
+PairP scaled_pair(PairP pp, float scale)
+{
+    pp.a *= scale;
+    pp.gamma *= scale;
+    pp.sig_dt *= scale;
+    for (int t = 0; t < DPD_MAX_SPECIES * DPD_MAX_SPECIES; ++t) {
+        pp.sa[t] *= scale;
+        pp.sg[t] *= scale;
+        pp.ss[t] *= scale;
+    }
+    return pp;
+}
+
 int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool record)
 {
     const int b = c->cur;
@@ -472,6 +485,9 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     }
     if (c->force_impl == 0 || c->dist) {
         const FixP fx = c->fix;
+        // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
+        // by the power-of-two scale (exact), so one FFMA per component quantises
+        const PairP pp = scaled_pair(c->pp, fx.scale);
         const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
                           ((g.n[2] + FT_BZ - 1) / FT_BZ);
         const size_t smem = sizeof(ForceTileSmem);

@@ -114,6 +114,13 @@ __device__ __forceinline__ float4 ldv(const ForceTileSmem &S, int j)
     return make_float4(v.x, v.y, v.z, __int_as_float(KMODE == 3 ? w_species(v.w) : 0));
 }
 
+// The tiled kernel's PairP is pre-scaled by FixP::scale (capi scaled_pair), so a pair scalar
+// s is already in fixed-point units and q = rint(d * s) is one FFMA per component.
+__device__ __forceinline__ int fix_q(float d, float s)
+{
+    return __float_as_int(__fmaf_rn(d, s, 12582912.0f)) - 0x4B400000;
+}
+
 __device__ __forceinline__ int to_fixed(float f, float scale)
 {
     // round-to-nearest via the 1.5 * 2^23 magic constant; valid for |f * scale| < 2^22
@@ -260,7 +267,7 @@ __device__ __forceinline__ float pair_eval(const PairP &pp, const FixP &fx, floa
     float s = 0.0f;
     if (r2 > 0.0f) {
         s = pair_scalar<KMODE>(pp, r2, dvdot, idi, idj, ks, vi.w, vj.w);
-        if (fabsf(s) * (r2 * rsqrtf(r2)) > fx.mag_lim) raise_err(err, ERR_RANGE, (int)idi);
+        if (fabsf(s) * (r2 * rsqrtf(r2)) > fx.mag_lim * fx.scale) raise_err(err, ERR_RANGE, (int)idi);
         if constexpr (RECORD) {
             const unsigned long long k = atomicAdd(rec.count, 1ull);
             if ((long long)k < rec.cap) {
@@ -367,7 +374,7 @@ __device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
 __device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &S, int j, float s, float dx, float dy,
                                                   float dz, float scale)
 {
-    const int qx = to_fixed(s * dx, scale), qy = to_fixed(s * dy, scale), qz = to_fixed(s * dz, scale);
+    const int qx = fix_q(dx, s), qy = fix_q(dy, s), qz = fix_q(dz, s);
     c.fx += qx;
     c.fy += qy;
     c.fz += qz;
@@ -381,7 +388,8 @@ __device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &
 template <bool RECORD, int KMODE>
 __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *frc,
                               const int *__restrict__ start, const Geom &g, const PairP &pp, const FixP &fx,
-                              uint32_t ks, PairRec &rec, int *err, int x0, int y0, int z0, int bx, int by, int bz)
+                              uint32_t ks, PairRec &rec, int *err, int x0, int y0, int z0, int bx, int by, int bz,
+                              float to_force)
 {
     // home particle h of the tile -> (home cell, slot) by a scan over the <= 32 home cells
     int nh = 0;
@@ -423,7 +431,9 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
                     const float r2 = (pi.x - pj.x) * (pi.x - pj.x) + (pi.y - pj.y) * (pi.y - pj.y) +
                                      (pi.z - pj.z) * (pi.z - pj.z);
                     if (!(r2 < pp.rc2)) continue;
-                    const float s = pair_eval<RECORD, KMODE>(pp, fx, pi, vi, pj, vel[j], ks, rec, err, dx, dy, dz);
+                    // to_force: 1 / scale when pp is in fixed-point units (tiled kernel), else 1
+                    const float s = to_force *
+                                    pair_eval<RECORD, KMODE>(pp, fx, pi, vi, pj, vel[j], ks, rec, err, dx, dy, dz);
                     Fx += s * dx;
                     Fy += s * dy;
                     Fz += s * dz;
@@ -525,7 +535,8 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     const int nhome = S.hoff[by * bz];
     if (total > FT_SCAP || nhome > FT_HCAP) {
         if (tid == 0) atomicAdd(&err[total > FT_SCAP ? 4 : 5], 1); // fallback statistics
-        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, x0, y0, z0, bx, by, bz);
+        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, x0, y0, z0, bx, by, bz,
+                                     fx.inv_scale);
         return;
     }
 
@@ -626,8 +637,7 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
                         float dx, dy, dz;
                         const float s =
                             pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, a), ldv<KMODE>(S, a), ks, rec, err, dx, dy, dz);
-                        const int qx = to_fixed(s * dx, fx.scale), qy = to_fixed(s * dy, fx.scale),
-                                  qz = to_fixed(s * dz, fx.scale);
+                        const int qx = fix_q(dx, s), qy = fix_q(dy, s), qz = fix_q(dz, s);
                         atomicAdd(&S.acc[0][s_i], qx);
                         atomicAdd(&S.acc[1][s_i], qy);
                         atomicAdd(&S.acc[2][s_i], qz);
@@ -694,7 +704,7 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
             }
 #pragma unroll
             for (int k = 0; k < FT_NCUR; ++k) cursor_flush(cu[k], S);
-            if (amax > fx.mag_lim) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(cu[0].vi.w));
+            if (amax > fx.mag_lim * fx.scale) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(cu[0].vi.w));
         }
         __syncwarp(); // the lists and the owner table are rewritten by the next round
     }
