@@ -64,12 +64,9 @@ struct ForceTileSmem {
     int wrow[FT_NWARP * FT_WSTRIDE];             //   list base minus prefix
     int soff[FT_NSC + 1];                        // staged cell -> smem start (exclusive scan)
     int cgs[FT_NSC];                             // staged cell -> global start
-    int scnt[FT_NSC];                            // staged cell -> particle count
     int hoff[FT_NHROW + 1];                      // home row -> first home index (prefix)
-    int tile[4];                                 // x0, y0, z0 of this tile
     int total;                                   // staged particles
     int nown;                                    // owners with a non-empty list
-    int overflow;                                // a capacity was exceeded -> fallback
 };
 
 // Extended-grid coordinate of interior cell coordinate c in [-1, n]: split dimensions
@@ -456,79 +453,74 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
 
-    // ---- tile geometry (integer divisions once per CTA) --------------------------------
+    // ---- tile geometry: every thread decodes blockIdx (no barrier) -----------------------
     static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
-    if (tid == 0) {
-        const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
-        const int b = blockIdx.x;
-        S.tile[0] = (b % ntx) * FT_BX;
-        S.tile[1] = ((b / ntx) % nty) * FT_BY;
-        S.tile[2] = (b / (ntx * nty)) * FT_BZ;
-        S.overflow = 0;
-    }
-    __syncthreads();
-    const int x0 = S.tile[0], y0 = S.tile[1], z0 = S.tile[2];
+    const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
+    const int x0 = (blockIdx.x % ntx) * FT_BX, y0 = ((blockIdx.x / ntx) % nty) * FT_BY,
+              z0 = (blockIdx.x / (ntx * nty)) * FT_BZ;
     const int bx = min(FT_BX, g.n[0] - x0), by = min(FT_BY, g.n[1] - y0), bz = min(FT_BZ, g.n[2] - z0);
     const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
     const int nsc = sxa * sya * sza;
 
-    // ---- 1a. staged cell table (counts, then one-warp exclusive scan) -----------------
-    for (int row = warp; row < sya * sza; row += FT_NWARP) {
-        const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0); // sza <= 3
-        const int ly = row - lz * sya;
-        // extended-grid coordinates: split dimensions index the halo ring (empty in the
-        // local lists) without wrapping; periodic-local dimensions wrap
-        const int gy = ext_coord(y0 - 1 + ly, g.n[1], g.split[1]);
-        const int gz = ext_coord(z0 + lz, g.n[2], g.split[2]);
-        if (lane < sxa) {
-            const int gx = ext_coord(x0 - 1 + lane, g.n[0], g.split[0]);
-            const int gc = gx + g.ext[0] * (gy + g.ext[1] * gz);
-            const int a = start[gc];
-            const int c = row * sxa + lane;
-            S.cgs[c] = a;
-            S.soff[c] = start[gc + 1] - a;
-            S.scnt[c] = start[gc + 1] - a;
-        }
-    }
-    __syncthreads();
+    // ---- 1a. staged cell table straight from global memory, one barrier: warp 0 takes one
+    //          staged row per lane (its cells' starts and counts, a warp scan of the row
+    //          sums, the in-row prefix); warp 1 takes one home row per lane (two loads: the
+    //          home cells of a row are contiguous in the extended grid) and scans them
+    static_assert(FT_SY * FT_SZ <= 32 && FT_NHROW <= 32, "one lane per row");
     if (warp == 0) {
-        constexpr int PER = (FT_NSC + 31) / 32;
-        int v[PER], sum = 0;
+        const int nrows = sya * sza;
+        int cnt[FT_SX], gst[FT_SX], rsum = 0;
+        if (lane < nrows) {
+            const int lz = lane >= 2 * sya ? 2 : (lane >= sya ? 1 : 0); // sza <= 3
+            const int ly = lane - lz * sya;
+            // extended-grid coordinates: split dimensions index the halo ring (empty in the
+            // local lists) without wrapping; periodic-local dimensions wrap
+            const int gy = ext_coord(y0 - 1 + ly, g.n[1], g.split[1]);
+            const int gz = ext_coord(z0 + lz, g.n[2], g.split[2]);
+            const int base = g.ext[0] * (gy + g.ext[1] * gz);
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int c = lane * PER + k;
-            v[k] = c < nsc ? S.soff[c] : 0;
-            sum += v[k];
+            for (int x = 0; x < FT_SX; ++x) {
+                cnt[x] = gst[x] = 0;
+                if (x < sxa) {
+                    const int gc = ext_coord(x0 - 1 + x, g.n[0], g.split[0]) + base;
+                    gst[x] = start[gc];
+                    cnt[x] = start[gc + 1] - gst[x];
+                    rsum += cnt[x];
+                }
+            }
         }
-        int incl = sum;
+        const int incl = warp_incl_scan(rsum, lane);
+        if (lane < nrows) {
+            int run = incl - rsum;
+            const int c0 = lane * sxa;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            for (int x = 0; x < FT_SX; ++x) {
+                if (x < sxa) {
+                    S.soff[c0 + x] = run;
+                    S.cgs[c0 + x] = gst[x];
+                    run += cnt[x];
+                }
+            }
         }
-        int run = incl - sum;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int c = lane * PER + k;
-            if (c < nsc) S.soff[c] = run;
-            run += v[k];
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) {
+            S.soff[nsc] = tot;
+            S.total = tot;
         }
-        if (lane == 31) {
-            S.soff[nsc] = incl;
-            S.total = incl;
+    } else if (warp == 1) {
+        const int nr = by * bz;
+        int sz = 0;
+        if (lane < nr) {
+            const int lz = lane >= by ? 1 : 0;
+            const int ly = 1 + lane - lz * by;
+            const int base = g.ext[0] * (ext_coord(y0 - 1 + ly, g.n[1], g.split[1]) +
+                                         g.ext[1] * ext_coord(z0 + lz, g.n[2], g.split[2]));
+            const int ga = ext_coord(x0, g.n[0], g.split[0]) + base; // x0 .. x0 + bx - 1: no wrap
+            sz = start[ga + bx] - start[ga];
         }
-    } else if (warp == 1 && lane == 0) {
-        // home rows (ly = 1..by, lz = 0..bz-1), cells lx = 1..bx: prefix of their sizes
-        // (from the counts; the in-place scan of soff runs concurrently in warp 0)
-        int run = 0;
-        for (int r = 0; r < by * bz; ++r) {
-            const int lz = r >= by ? 1 : 0;
-            const int ly = 1 + r - lz * by;
-            const int c = 1 + sxa * (ly + sya * lz);
-            S.hoff[r] = run;
-            for (int x = 0; x < bx; ++x) run += S.scnt[c + x];
-        }
-        S.hoff[by * bz] = run;
+        const int incl = warp_incl_scan(sz, lane);
+        if (lane < nr) S.hoff[lane] = incl - sz;
+        if (lane == nr - 1) S.hoff[nr] = incl;
     }
     __syncthreads();
     const int total = S.total;
