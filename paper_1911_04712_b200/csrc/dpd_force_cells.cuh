@@ -38,7 +38,6 @@ struct ForceCellSmem {
     int wrow[FC_NWARP][32];                      //   list base minus prefix
     int soff[FT_NSC + 1];                        // staged cell -> smem start
     int cgs[FT_NSC];                             // staged cell -> global start
-    int tile[4];
     int total;
     int next_task;
 };
@@ -182,17 +181,11 @@ __global__ void __launch_bounds__(FC_NTHR, 3)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
 
-    // ---- tile geometry ----------------------------------------------------------------
-    if (tid == 0) {
-        const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
-        const int b = blockIdx.x;
-        S.tile[0] = (b % ntx) * FT_BX;
-        S.tile[1] = ((b / ntx) % nty) * FT_BY;
-        S.tile[2] = (b / (ntx * nty)) * FT_BZ;
-        S.next_task = 0;
-    }
-    __syncthreads();
-    const int x0 = S.tile[0], y0 = S.tile[1], z0 = S.tile[2];
+    // ---- tile geometry: every thread decodes blockIdx ----------------------------------
+    const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
+    const int x0 = (blockIdx.x % ntx) * FT_BX, y0 = ((blockIdx.x / ntx) % nty) * FT_BY,
+              z0 = (blockIdx.x / (ntx * nty)) * FT_BZ;
+    if (tid == 0) S.next_task = 0; // read only after the barriers below
     const int bx = min(FT_BX, g.n[0] - x0), by = min(FT_BY, g.n[1] - y0), bz = min(FT_BZ, g.n[2] - z0);
     const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
     const int nsc = sxa * sya * sza;

@@ -43,9 +43,16 @@ for r in rows:
     c["ins"] += num(r[hdr["Instructions Executed"]])
     c["tin"] += num(r[hdr["Thread Instructions Executed"]])
     c["wf"] += num(r[hdr["L1 Wavefronts Shared"]])
+    c["samp"] += num(r[hdr["Warp Stall Sampling (All Samples)"]])
+    for k, i in hdr.items():
+        if k.startswith("stall_") and "Not Issued" not in k:
+            c[k] += num(r[i])
 ti = sum(c["ins"] for c in agg.values())
 tw = sum(c["wf"] for c in agg.values())
+ts = sum(c["samp"] for c in agg.values())
 print(f"total warp-instr {ti/1e6:.1f}M  smem wavefronts {tw/1e6:.1f}M")
 for k, c in sorted(agg.items(), key=lambda kv: -kv[1]["ins"])[:n]:
+    st = sorted(((v, s[6:]) for s, v in c.items() if s.startswith("stall_")), reverse=True)[:3]
     print(f"{c['ins']/1e6:7.1f}M {100*c['ins']/ti:5.1f}%  lanes {c['tin']/max(1,c['ins']):4.1f}  "
-          f"wf {c['wf']/1e6:6.1f}M  {k}")
+          f"wf {c['wf']/1e6:6.1f}M  samples {100*c['samp']/max(1,ts):5.1f}% "
+          f"({' '.join(f'{n}:{100*v/max(1,c[chr(115)+chr(97)+chr(109)+chr(112)]):.0f}%' for v, n in st)})  {k}")

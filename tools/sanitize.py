@@ -1,5 +1,7 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
-config-1 box on one domain (both force kernels) and a 2x2x2 in-process group."""
+config-1 box on one domain (all three force kernels), the species matrix, asynchronous
+dumps (snapshot kernel + copy stream + writer thread) and a 2x2x2 in-process group."""
+import tempfile
 import os
 import sys
 
@@ -12,12 +14,22 @@ from paper_1911_04712_b200 import capi  # noqa: E402
 
 cfg = workloads.CONFIGS["parity"]
 pos, vel = workloads.make_config(cfg)
-for k in (0, 1):
+for k in (0, 1, 2):
     d = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
     d.set_option("force_kernel", k)
     d.set_particles(pos, vel)
     d.step(3)
     d.get_forces()
+d = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
+d.set_species(np.array([[25.0, 40.0], [40.0, 25.0]]), np.array([[45.0, 10.0], [10.0, 45.0]]))
+d.set_particles_typed(pos, vel, None, (np.arange(len(pos)) % 2).astype(np.int32))
+d.step(3)
+with tempfile.TemporaryDirectory() as tmp:
+    d.dump_open(os.path.join(tmp, "s"), 2)
+    d.dump_every(2)
+    d.step(5)
+    d.dump_now()
+    assert d.dump_close() == 4  # steps 4, 6, 8 and dump_now at 8
 big = workloads.with_box(cfg, (12.0, 12.0, 12.0))
 p2, v2 = workloads.make_config(big)
 ctxs = capi.dpd_create_group(big.box, big.rc, big.a, big.gamma, big.kT, big.power, big.dt, big.seed, (2, 2, 2))
