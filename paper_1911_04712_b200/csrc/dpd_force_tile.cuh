@@ -40,12 +40,22 @@ constexpr int kSweepUnroll = FT_SWEEP_UNROLL;
 #define FT_SEG_UNROLL 5 // unroll of the 5-segment loop of the sweep (measured: 1 -> 457, 5 -> 449 us)
 #endif
 constexpr int kSegUnroll = FT_SEG_UNROLL;
+#ifndef FT_STAGE_UNROLL
+#define FT_STAGE_UNROLL 1 // unroll of the per-lane staging copy / fix loops
+#endif
+constexpr int kStageUnroll = FT_STAGE_UNROLL;
+#ifndef FT_EXPECT
+#define FT_EXPECT 0 // owner switches of the pair cursors marked unlikely
+#endif
 
 constexpr int FT_BX = 4, FT_BY = 4, FT_BZ = 2;
 constexpr int FT_SX = FT_BX + 2, FT_SY = FT_BY + 2, FT_SZ = FT_BZ + 1;
 constexpr int FT_NSC = FT_SX * FT_SY * FT_SZ; // staged cells (108)
 constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
-constexpr int FT_NTHR = 288;                  // 9 warps: ~28 home particles each (balanced ranges)
+#ifndef FT_NTHR_DEF
+#define FT_NTHR_DEF 288
+#endif
+constexpr int FT_NTHR = FT_NTHR_DEF;          // 9 warps: ~28 home particles each (balanced ranges)
 constexpr int FT_NWARP = FT_NTHR / 32;
 constexpr int FT_SCAP = 1024;                 // staged particles (mean 864, sd 29 at rho = 8: 5.5 sd)
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
@@ -252,6 +262,7 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__restrict__ pos,
                                            const float4 *__restrict__ vel, int g0, int s0, int len, int lane)
 {
+#pragma unroll kStageUnroll
     for (int k = lane; k < len; k += 32) {
         cp_async16(reinterpret_cast<float4 *>(S.lst) + s0 + k, &pos[g0 + k]);
         cp_async16(&S.sv[s0 + k], &vel[g0 + k]);
@@ -263,6 +274,7 @@ __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__res
 template <int KMODE>
 __device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, float sx, float sy, float sz, int lane)
 {
+#pragma unroll kStageUnroll
     for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
         const float4 p = reinterpret_cast<const float4 *>(S.lst)[s];
@@ -400,7 +412,11 @@ __device__ __forceinline__ void cursor_flush(PairCursor &c, ForceTileSmem &S)
 // Entry t of the list (the partner j); moves to the next owner first when t crosses it.
 __device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
 {
+#if FT_EXPECT
+    if (__builtin_expect(c.t >= c.enext, 0)) { // next owner (never empty)
+#else
     if (c.t >= c.enext) { // next owner (never empty)
+#endif
         cursor_flush(c, S);
         ++c.o;
         cursor_load(c, S);
