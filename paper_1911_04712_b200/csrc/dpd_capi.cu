@@ -436,6 +436,23 @@ int phase_ghost_pack(dpd_ctx *c)
 }
 
 // a5: local-local pairs at RNG step index `step`.
+// Host Philox2x32-10 (C-7) for the per-step key: k_s = word 0 of
+// Philox2x32-10({s lo, s hi}, seed lo ^ seed hi); the tiled kernel receives the ten round
+// keys k_s + r W as a parameter (dpd_device.cuh RoundKeys).
+RoundKeys host_round_keys(uint32_t s_lo, uint32_t s_hi, uint32_t seed_fold)
+{
+    uint32_t c0 = s_lo, c1 = s_hi, k = seed_fold;
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t prod = (uint64_t)kPhilox2M * c0;
+        c0 = (uint32_t)(prod >> 32) ^ k ^ c1;
+        c1 = (uint32_t)prod;
+        k += kPhilox2W;
+    }
+    RoundKeys K;
+    for (int r = 0; r < 10; ++r) K.k[r] = c0 + (uint32_t)r * kPhilox2W;
+    return K;
+}
+
 PairP scaled_pair(PairP pp, float scale)
 {
     pp.a *= scale;
@@ -488,14 +505,15 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
         // by the power-of-two scale (exact), so one FFMA per component quantises
         const PairP pp = scaled_pair(c->pp, fx.scale);
+        const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp.seed_fold);
         const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
                           ((g.n[2] + FT_BZ - 1) / FT_BZ);
         const size_t smem = sizeof(ForceTileSmem);
         const int *st = c->start[c->scur].p;
         return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
 #define DPD_TILE(R, K)                                                                                              \
-    k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, s_lo, \
-                                                            s_hi, rec, c->err.p)
+    k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, \
+                                                            c->err.p)
             if (record) {
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;

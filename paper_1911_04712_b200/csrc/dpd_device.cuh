@@ -93,6 +93,33 @@ __device__ __forceinline__ uint2 pair_words(uint32_t ida, uint32_t idb, uint32_t
     return philox2x32_10(min(ida, idb), max(ida, idb), ks);
 }
 
+// The ten round keys k_s + r W of one step, computed once on the host: as a kernel
+// parameter they sit in the constant bank and feed the round's LOP3 directly (no per-pair
+// key schedule).
+struct RoundKeys {
+    uint32_t k[10];
+};
+
+__device__ __forceinline__ uint2 pair_words(uint32_t ida, uint32_t idb, const RoundKeys &K)
+{
+    uint32_t c0 = min(ida, idb), c1 = max(ida, idb);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi = __umulhi(kPhilox2M, c0), lo = kPhilox2M * c0;
+        c0 = hi ^ K.k[r] ^ c1;
+        c1 = lo;
+    }
+    return make_uint2(c0, c1);
+}
+
+__device__ __forceinline__ RoundKeys round_keys(uint32_t ks)
+{
+    RoundKeys K;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) K.k[r] = ks + (uint32_t)r * kPhilox2W;
+    return K;
+}
+
 __device__ __forceinline__ float sqrt_approx(float x)
 {
     float y;
@@ -135,9 +162,9 @@ __device__ __forceinline__ float weight_R(float w, float k)
 // r2 in (0, rc2) assumed.  KMODE 0: k = 1/2, 1: k = 1, 2: generic k, 3: generic k with the
 // species matrix (a, gamma, sigma of the pair looked up from the species ti, tj).
 // pp.sig_dt / pp.ss hold sigma/sqrt(dt) * kBM (box_muller_s convention).
-template <int KMODE>
+template <int KMODE, class KeyT>
 __device__ __forceinline__ float pair_mag(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
-                                          uint32_t ks, int ti, int tj, float &mag)
+                                          const KeyT &ks, int ti, int tj, float &mag)
 {
     float a = pp.a, gamma = pp.gamma, sig_dt = pp.sig_dt;
     if constexpr (KMODE == 3) {
@@ -159,9 +186,9 @@ __device__ __forceinline__ float pair_mag(const PairP &pp, float r2, float dvdot
     return mag * rinv;
 }
 
-template <int KMODE>
+template <int KMODE, class KeyT>
 __device__ __forceinline__ float pair_scalar(const PairP &pp, float r2, float dvdot, uint32_t idi, uint32_t idj,
-                                             uint32_t ks, float vwi, float vwj)
+                                             const KeyT &ks, float vwi, float vwj)
 {
     float mag;
     return pair_mag<KMODE>(pp, r2, dvdot, idi, idj, ks, __float_as_int(vwi), __float_as_int(vwj), mag);

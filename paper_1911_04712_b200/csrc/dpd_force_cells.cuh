@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(FC_NTHR, 3)
     const int total = S.total;
     if (total > FC_SCAP) {
         if (tid == 0) atomicAdd(&err[4], 1); // fallback statistics
-        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, x0, y0, z0, bx, by, bz, 1.0f);
+        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, round_keys(ks), rec, err, x0, y0, z0, bx, by, bz, 1.0f);
         return;
     }
 

@@ -304,7 +304,7 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane)
 // Pair evaluation shared by the fast path (smem operands) and the record path.
 template <bool RECORD, int KMODE>
 __device__ __forceinline__ float pair_eval(const PairP &pp, const FixP &fx, float4 pi, float4 vi, float4 pj,
-                                           float4 vj, uint32_t ks, PairRec &rec, int *err, float &dx, float &dy,
+                                           float4 vj, const RoundKeys &ks, PairRec &rec, int *err, float &dx, float &dy,
                                            float &dz)
 {
     dx = pi.x - pj.x;
@@ -334,7 +334,7 @@ __device__ __forceinline__ float pair_eval(const PairP &pp, const FixP &fx, floa
 // The largest |mag| seen is kept in amax and range-checked once per walk.
 template <int KMODE>
 __device__ __forceinline__ float pair_core(const PairP &pp, float pix, float piy, float piz, float4 vi, float pjx,
-                                           float pjy, float pjz, float4 vj, uint32_t ks, float &dx, float &dy,
+                                           float pjy, float pjz, float4 vj, const RoundKeys &ks, float &dx, float &dy,
                                            float &dz, float &amax)
 {
     dx = pix - pjx;
@@ -351,7 +351,7 @@ __device__ __forceinline__ float pair_core(const PairP &pp, float pix, float piy
 
 // Debug pair recording (RECORD instantiation only).
 template <int KMODE>
-__device__ __forceinline__ void pair_record(float4 vi, float4 vj, float dx, float dy, float dz, uint32_t ks,
+__device__ __forceinline__ void pair_record(float4 vi, float4 vj, float dx, float dy, float dz, const RoundKeys &ks,
                                             PairRec &rec)
 {
     if (dx * dx + dy * dy + dz * dz > 0.0f) {
@@ -441,7 +441,7 @@ __device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &
 template <bool RECORD, int KMODE>
 __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *frc,
                               const int *__restrict__ start, const Geom &g, const PairP &pp, const FixP &fx,
-                              uint32_t ks, PairRec &rec, int *err, int x0, int y0, int z0, int bx, int by, int bz,
+                              const RoundKeys &ks, PairRec &rec, int *err, int x0, int y0, int z0, int bx, int by, int bz,
                               float to_force)
 {
     // home particle h of the tile -> (home cell, slot) by a scan over the <= 32 home cells
@@ -501,13 +501,13 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
 template <bool RECORD, int KMODE>
 __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
-                 const int *__restrict__ start, Geom g, PairP pp, FixP fx, uint32_t s_lo, uint32_t s_hi,
+                 const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
                  PairRec rec, int *err)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
+    const RoundKeys &ks = rk; // host-computed round keys of this step (constant bank)
 
     // ---- tile geometry: every thread decodes blockIdx (no barrier) -----------------------
     static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
