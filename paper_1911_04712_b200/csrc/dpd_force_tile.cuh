@@ -85,9 +85,8 @@ struct ForceTileSmem {
                                               // during staging: the AoS landing buffer of the positions
     float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // staged positions (tile frame), SoA
     int acc[3][FT_SCAP];                         // fixed-point force sums
-    int woex[FT_NWARP * FT_WSTRIDE];             // per warp: compacted owners' list prefix (+ total)
-    int wsi[FT_NWARP * FT_WSTRIDE];              //   staged index of the owner
-    int wrow[FT_NWARP * FT_WSTRIDE];             //   list base minus prefix
+    int4 wrec[FT_NWARP * FT_WSTRIDE];            // per warp, compacted owners: {list prefix, prefix + count,
+                                                 //   list base minus prefix, staged index} (one LDS.128)
     int soff[FT_NSC + 1];                        // staged cell -> smem start (exclusive scan)
     int cgs[FT_NSC];                             // staged cell -> global start
     int hoff[FT_NHROW + 1];                      // home row -> first home index (prefix)
@@ -367,7 +366,7 @@ __device__ __forceinline__ void pair_record(float4 vi, float4 vj, float dx, floa
 // Walk over a contiguous range [t, t1) of one warp's concatenated pair lists.  Owners (home
 // particles with a non-empty list) change at most a few times per range; the i-side
 // fixed-point sum is kept in registers and flushed on each owner change.  `o` indexes the
-// warp's owner table (woex/wsi/wrow at stride FT_WSTRIDE).
+// warp's owner table (wrec at stride FT_WSTRIDE).
 struct PairCursor {
     int t, t1, o, enext, si, lrow;
     float px, py, pz;
@@ -377,9 +376,10 @@ struct PairCursor {
 
 __device__ __forceinline__ void cursor_load(PairCursor &c, const ForceTileSmem &S)
 {
-    c.si = S.wsi[c.o];
-    c.lrow = S.wrow[c.o];
-    c.enext = S.woex[c.o + 1];
+    const int4 r = S.wrec[c.o];
+    c.enext = r.y;
+    c.lrow = r.z;
+    c.si = r.w;
     c.px = S.sx[c.si];
     c.py = S.sy[c.si];
     c.pz = S.sz[c.si];
@@ -391,10 +391,10 @@ __device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &
     c.t = t0;
     c.t1 = t1;
     c.fx = c.fy = c.fz = 0;
-    int o = 0; // largest owner slot with woex[o] <= t0
+    int o = 0; // largest owner slot whose list prefix is <= t0
 #pragma unroll
     for (int step = 16; step > 0; step >>= 1)
-        if (o + step < nown && S.woex[base + o + step] <= t0) o += step;
+        if (o + step < nown && S.wrec[base + o + step].x <= t0) o += step;
     c.o = base + o;
     cursor_load(c, S);
 }
@@ -706,11 +706,8 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
         const int nown = tp & 0xFF, tot = tp >> 8;
         if (cnt > 0) {
             const int o = (incl - v) & 0xFF, e = (incl - v) >> 8;
-            S.woex[wb + o] = e;
-            S.wsi[wb + o] = s_i;
-            S.wrow[wb + o] = tid * FT_LSTRIDE - e;
+            S.wrec[wb + o] = make_int4(e, e + cnt, tid * FT_LSTRIDE - e, s_i);
         }
-        if (lane == 0) S.woex[wb + nown] = tot;
         __syncwarp();
 
         // ---- 4. pair evaluation: contiguous chunk of the warp's lists per lane, walked by two
