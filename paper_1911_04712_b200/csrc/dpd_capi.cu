@@ -149,6 +149,8 @@ struct dpd_ctx {
     float wprm[DPD_MAX_WALLS][4] = {};
     float wvel[DPD_MAX_WALLS][3] = {};
     int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel, 2: cell-warp
+    int tile_persistent = 0; // tiled kernel as resident CTAs walking the tiles (option "tile_persistent")
+    int nsm = 148;
     Geom geom{};
     PairP pp{};
     FixP fix{};
@@ -512,8 +514,14 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         const int *st = c->start[c->scur].p;
         return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
 #define DPD_TILE(R, K)                                                                                              \
-    k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, \
-                                                            c->err.p)
+    do {                                                                                                            \
+        if (c->tile_persistent)                                                                                     \
+            k_force_tile_p<R, K><<<std::min(ntile, c->nsm * 3), FT_NTHR, smem, c->stream>>>(                        \
+                c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, c->err.p);                               \
+        else                                                                                                        \
+            k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp,   \
+                                                                    fx, rk, rec, c->err.p);                         \
+    } while (0)
             if (record) {
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;
@@ -1051,10 +1059,17 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     {
         // two tiles per SM need the maximum shared-memory carveout (2 x (smem + 1 KB) <= 228 KB)
         const int smem = (int)sizeof(ForceTileSmem);
-        const void *fns[8] = {(const void *)k_force_tile<false, 0>, (const void *)k_force_tile<false, 1>,
-                              (const void *)k_force_tile<false, 2>, (const void *)k_force_tile<false, 3>,
-                              (const void *)k_force_tile<true, 0>,  (const void *)k_force_tile<true, 1>,
-                              (const void *)k_force_tile<true, 2>,  (const void *)k_force_tile<true, 3>};
+        const void *fns[16] = {(const void *)k_force_tile<false, 0>,   (const void *)k_force_tile<false, 1>,
+                               (const void *)k_force_tile<false, 2>,   (const void *)k_force_tile<false, 3>,
+                               (const void *)k_force_tile<true, 0>,    (const void *)k_force_tile<true, 1>,
+                               (const void *)k_force_tile<true, 2>,    (const void *)k_force_tile<true, 3>,
+                               (const void *)k_force_tile_p<false, 0>, (const void *)k_force_tile_p<false, 1>,
+                               (const void *)k_force_tile_p<false, 2>, (const void *)k_force_tile_p<false, 3>,
+                               (const void *)k_force_tile_p<true, 0>,  (const void *)k_force_tile_p<true, 1>,
+                               (const void *)k_force_tile_p<true, 2>,  (const void *)k_force_tile_p<true, 3>};
+        int dev = 0;
+        CUDA_TRY(c, cudaGetDevice(&dev));
+        CUDA_TRY(c, cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
         for (const void *f : fns) {
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1257,6 +1272,11 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
             return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled), 1 (reference) or 2 (cell-warp)");
         if (value != 0 && c->dist) return fail(c, DPD_ERR_ARG, "force_kernel %d is single-domain only", (int)value);
         c->force_impl = (int)value;
+        return DPD_OK;
+    }
+    if (strcmp(name, "tile_persistent") == 0) {
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "tile_persistent must be 0 or 1");
+        c->tile_persistent = (int)value;
         return DPD_OK;
     }
     if (strcmp(name, "body_force_mode") == 0) {

@@ -79,6 +79,15 @@ struct FixP {
     int prune;       // row-end pruning on (1, default) / off (0): engine option "row_pruning"
 };
 
+// Cell table of one tile (SURVEY §8a row a5 staging): staged cell -> smem / global start,
+// home rows -> first home index, staged particle count.
+struct TileTab {
+    int soff[FT_NSC + 1]; // staged cell -> smem start (exclusive scan)
+    int cgs[FT_NSC];      // staged cell -> global start
+    int hoff[FT_NHROW + 1]; // home row -> first home index (prefix)
+    int total;            // staged particles
+};
+
 struct ForceTileSmem {
     float4 sv[FT_SCAP];                       // staged velocities; w: id bits | species << 30 (stage_fix)
     unsigned short lst[FT_NTHR * FT_LSTRIDE]; // per-thread pair lists (one home particle each);
@@ -87,10 +96,8 @@ struct ForceTileSmem {
     int acc[3][FT_SCAP];                         // fixed-point force sums
     int4 wrec[FT_NWARP * FT_WSTRIDE];            // per warp, compacted owners: {list prefix, prefix + count,
                                                  //   list base minus prefix, staged index} (one LDS.128)
-    int soff[FT_NSC + 1];                        // staged cell -> smem start (exclusive scan)
-    int cgs[FT_NSC];                             // staged cell -> global start
-    int hoff[FT_NHROW + 1];                      // home row -> first home index (prefix)
-    int total;                                   // staged particles
+    TileTab tab[2];                              // cell tables: current tile / next tile (persistent)
+    int done_cnt;                                // persistent kernel: warps done with their pairs
     int nown;                                    // owners with a non-empty list
 };
 
@@ -498,32 +505,44 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
     }
 }
 
-template <bool RECORD, int KMODE>
-__global__ void __launch_bounds__(FT_NTHR, FT_MINB)
-    k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
-                 const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
-                 PairRec rec, int *err)
+// ---------------------------------------------------------------------------------------
+// Tile phases (shared by the one-tile-per-CTA kernel and the persistent kernel).
+// ---------------------------------------------------------------------------------------
+struct TileGeo {
+    int x0, y0, z0, bx, by, bz;
+};
+
+__device__ __forceinline__ TileGeo tile_geo(int t, const Geom &g)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const RoundKeys &ks = rk; // host-computed round keys of this step (constant bank)
-
-    // ---- tile geometry: every thread decodes blockIdx (no barrier) -----------------------
-    static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
     const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
-    const int x0 = (blockIdx.x % ntx) * FT_BX, y0 = ((blockIdx.x / ntx) % nty) * FT_BY,
-              z0 = (blockIdx.x / (ntx * nty)) * FT_BZ;
-    const int bx = min(FT_BX, g.n[0] - x0), by = min(FT_BY, g.n[1] - y0), bz = min(FT_BZ, g.n[2] - z0);
-    const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
-    const int nsc = sxa * sya * sza;
+    TileGeo G;
+    G.x0 = (t % ntx) * FT_BX;
+    G.y0 = ((t / ntx) % nty) * FT_BY;
+    G.z0 = (t / (ntx * nty)) * FT_BZ;
+    G.bx = min(FT_BX, g.n[0] - G.x0);
+    G.by = min(FT_BY, g.n[1] - G.y0);
+    G.bz = min(FT_BZ, g.n[2] - G.z0);
+    return G;
+}
 
-    // ---- 1a. staged cell table straight from global memory, one barrier: warp 0 takes one
-    //          staged row per lane (its cells' starts and counts, a warp scan of the row
-    //          sums, the in-row prefix); warp 1 takes one home row per lane (two loads: the
-    //          home cells of a row are contiguous in the extended grid) and scans them
+__device__ __forceinline__ int tile_count(const Geom &g)
+{
+    return ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) * ((g.n[2] + FT_BZ - 1) / FT_BZ);
+}
+
+// 1a. staged cell table straight from global memory.  role 0 (one warp): one staged row per
+// lane -- its cells' starts and counts, a warp scan of the row sums, the in-row prefix;
+// role 1 (another warp): one home row per lane (two loads: the home cells of a row are
+// contiguous in the extended grid) and their scan.
+__device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const Geom &g,
+                                           const int *__restrict__ start, int role, int lane)
+{
+    const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
+    const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
+    (void)x0; (void)y0; (void)z0; (void)sza;
+    const int nsc = sxa * sya * sza;
     static_assert(FT_SY * FT_SZ <= 32 && FT_NHROW <= 32, "one lane per row");
-    if (warp == 0) {
+    if (role == 0) {
         const int nrows = sya * sza;
         int cnt[FT_SX], gst[FT_SX], rsum = 0;
         if (lane < nrows) {
@@ -552,18 +571,18 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
 #pragma unroll
             for (int x = 0; x < FT_SX; ++x) {
                 if (x < sxa) {
-                    S.soff[c0 + x] = run;
-                    S.cgs[c0 + x] = gst[x];
+                    T.soff[c0 + x] = run;
+                    T.cgs[c0 + x] = gst[x];
                     run += cnt[x];
                 }
             }
         }
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
         if (lane == 0) {
-            S.soff[nsc] = tot;
-            S.total = tot;
+            T.soff[nsc] = tot;
+            T.total = tot;
         }
-    } else if (warp == 1) {
+    } else {
         const int nr = by * bz;
         int sz = 0;
         if (lane < nr) {
@@ -575,33 +594,40 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
             sz = start[ga + bx] - start[ga];
         }
         const int incl = warp_incl_scan(sz, lane);
-        if (lane < nr) S.hoff[lane] = incl - sz;
-        if (lane == nr - 1) S.hoff[nr] = incl;
+        if (lane < nr) T.hoff[lane] = incl - sz;
+        if (lane == nr - 1) T.hoff[nr] = incl;
     }
-    __syncthreads();
-    const int total = S.total;
-    const int nhome = S.hoff[by * bz];
-    if (total > FT_SCAP || nhome > FT_HCAP) {
-        if (tid == 0) atomicAdd(&err[total > FT_SCAP ? 4 : 5], 1); // fallback statistics
-        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, x0, y0, z0, bx, by, bz,
-                                     fx.inv_scale);
-        return;
-    }
+}
 
-    // ---- 1b. stage rows: each row is <= 3 contiguous global segments; all copies of the
-    //          warp are issued first (async), then each row is shifted / transposed
+// 1b. issue the staging copies of this warp's rows (cp.async, not waited for).
+__device__ __forceinline__ void tile_stage_issue(ForceTileSmem &S, const TileTab &T, const TileGeo &G,
+                                                 const Geom &g, const float4 *__restrict__ pos,
+                                                 const float4 *__restrict__ vel, int warp, int lane)
+{
+    const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
+    const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
+    (void)x0; (void)y0; (void)z0; (void)sza;
     const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int c0 = sxa * row; // lx = 0
         // segment A: lx = 0; B: lx = 1..bx; C: lx = bx + 1 (merged when not wrapped)
-        const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
+        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.soff[c0 + bx + 2];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
-        if (wrap_lo) stage_copy(S, pos, vel, S.cgs[c0], a0, b0 - a0, lane);
-        stage_copy(S, pos, vel, wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0], mlo, mhi - mlo, lane);
-        if (wrap_hi) stage_copy(S, pos, vel, S.cgs[c0 + bx + 1], c0s, e0 - c0s, lane);
+        if (wrap_lo) stage_copy(S, pos, vel, T.cgs[c0], a0, b0 - a0, lane);
+        stage_copy(S, pos, vel, wrap_lo ? T.cgs[c0 + 1] : T.cgs[c0], mlo, mhi - mlo, lane);
+        if (wrap_hi) stage_copy(S, pos, vel, T.cgs[c0 + bx + 1], c0s, e0 - c0s, lane);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
+}
+
+// 1b (second half, after cp.async.wait_all): periodic shift, SoA copy, ids, zeroed sums.
+template <int KMODE>
+__device__ __forceinline__ void tile_stage_fix(ForceTileSmem &S, const TileTab &T, const TileGeo &G, const Geom &g,
+                                               int warp, int lane)
+{
+    const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
+    const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
+    (void)x0; (void)y0; (void)z0; (void)sza;
+    const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int lz = row >= 2 * sya ? 2 : (row >= sya ? 1 : 0);
         const int ly = row - lz * sya;
@@ -609,14 +635,24 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
         const float sy = g.split[1] ? 0.0f : (gy < 0 ? -g.L[1] : (gy >= g.n[1] ? g.L[1] : 0.0f));
         const float sz = g.split[2] ? 0.0f : (gz >= g.n[2] ? g.L[2] : 0.0f);
         const int c0 = sxa * row;
-        const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
+        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.soff[c0 + bx + 2];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
         if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
         stage_fix<KMODE>(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
         if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
     }
-    __syncthreads();
+}
 
+// 2-4. sweep + pairs of this warp's home particles.
+template <bool RECORD, int KMODE>
+__device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, const TileGeo &G, const Geom &g,
+                                           const PairP &pp, const FixP &fx, const RoundKeys &ks, PairRec &rec,
+                                           int *err, int tid, int warp, int lane)
+{
+    const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
+    const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
+    (void)x0; (void)y0; (void)z0; (void)sza;
+    const int nhome = T.hoff[by * bz];
     // ---- 2-4. per warp, one home particle per lane (a second round only past FT_NTHR):
     //           sweep the lane's 5 segments into its list, then evaluate the warp's pairs
     //           with a warp-balanced split -- no CTA barrier between sweep and pairs
@@ -632,13 +668,13 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
         int cnt = 0, s_i = 0;
         if (h < hend) {
             int r = 0;
-            while (r + 1 < by * bz && S.hoff[r + 1] <= h) ++r;
+            while (r + 1 < by * bz && T.hoff[r + 1] <= h) ++r;
             const int lz = r >= by ? 1 : 0;
             const int ly = 1 + r - lz * by;
             const int crow = sxa * (ly + sya * lz);
-            s_i = S.soff[crow + 1] + (h - S.hoff[r]);
+            s_i = T.soff[crow + 1] + (h - T.hoff[r]);
             int lx = 1;
-            while (lx < bx && S.soff[crow + lx + 1] <= s_i) ++lx;
+            while (lx < bx && T.soff[crow + lx + 1] <= s_i) ++lx;
             const int c = crow + lx;
             const int c1 = c - 1 + sxa; // (lx - 1, ly + 1, lz): the y+1 row
             const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
@@ -655,15 +691,15 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
             for (int k = 0; k < 5; ++k) {
                 // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
                 const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
-                int a = (k == 0) ? s_i + 1 : S.soff[cs];
-                int b = S.soff[cs + (k == 0 ? 2 : 3)];
+                int a = (k == 0) ? s_i + 1 : T.soff[cs];
+                int b = T.soff[cs + (k == 0 ? 2 : 3)];
                 if (k > 0 && fx.prune) {
                     const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
                     const float qz = (k == 1) ? 0.0f : dzr;
                     const float q = qy * qy + qz * qz;
                     if (!(q < pp.rc2)) continue;
-                    if (!(dxl * dxl + q < pp.rc2)) a = S.soff[cs + 1];
-                    if (!(dxr * dxr + q < pp.rc2)) b = S.soff[cs + 2];
+                    if (!(dxl * dxl + q < pp.rc2)) a = T.soff[cs + 1];
+                    if (!(dxr * dxr + q < pp.rc2)) b = T.soff[cs + 2];
                 }
                 // a chunk of m candidates adds at most m entries: sweep in chunks that fit the
                 // remaining list capacity; once the list is full (first particle of a crowded
@@ -753,23 +789,132 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
         }
         __syncwarp(); // the lists and the owner table are rewritten by the next round
     }
-    __syncthreads();
+}
 
-    // ---- 5. flush: fixed point -> fp32, one vector reduction per staged particle -------
-    // rows map back to <= 3 contiguous global segments, exactly as they were staged
+// 5. flush: fixed point -> fp32, one vector reduction per staged particle; rows map back
+// to <= 3 contiguous global segments, exactly as they were staged.
+__device__ __forceinline__ void tile_flush(const ForceTileSmem &S, const TileTab &T, const TileGeo &G,
+                                           const Geom &g, const FixP &fx, float4 *frc, int warp, int lane)
+{
+    const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
+    const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
+    (void)x0; (void)y0; (void)z0; (void)sza;
+    const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
         const int c0 = sxa * row;
-        const int a0 = S.soff[c0], b0 = S.soff[c0 + 1], c0s = S.soff[c0 + bx + 1], e0 = S.soff[c0 + bx + 2];
+        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.soff[c0 + bx + 2];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
-        const int gm = wrap_lo ? S.cgs[c0 + 1] : S.cgs[c0];
+        const int gm = wrap_lo ? T.cgs[c0 + 1] : T.cgs[c0];
         for (int s = a0 + lane; s < e0; s += 32) {
-            const int gi = (s < mlo) ? S.cgs[c0] + (s - a0)
-                                     : (s < mhi ? gm + (s - mlo) : S.cgs[c0 + bx + 1] + (s - c0s));
+            const int gi = (s < mlo) ? T.cgs[c0] + (s - a0)
+                                     : (s < mhi ? gm + (s - mlo) : T.cgs[c0 + bx + 1] + (s - c0s));
             const int qx = S.acc[0][s], qy = S.acc[1][s], qz = S.acc[2][s];
             if (qx | qy | qz)
                 atomicAdd(&frc[gi], make_float4((float)qx * fx.inv_scale, (float)qy * fx.inv_scale,
                                                 (float)qz * fx.inv_scale, 0.0f));
         }
+    }
+}
+
+__device__ __forceinline__ bool tile_overflows(const TileTab &T, const TileGeo &G)
+{
+    return T.total > FT_SCAP || T.hoff[G.by * G.bz] > FT_HCAP;
+}
+
+template <bool RECORD, int KMODE>
+__global__ void __launch_bounds__(FT_NTHR, FT_MINB)
+    k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
+                 const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
+                 PairRec rec, int *err)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const RoundKeys &ks = rk; // host-computed round keys of this step (constant bank)
+    static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
+    const TileGeo G = tile_geo(blockIdx.x, g);
+    TileTab &T = S.tab[0];
+    if (warp < 2) tile_table(T, G, g, start, warp, lane);
+    __syncthreads();
+    if (tile_overflows(T, G)) {
+        if (tid == 0) atomicAdd(&err[T.total > FT_SCAP ? 4 : 5], 1); // fallback statistics
+        tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, G.x0, G.y0, G.z0, G.bx, G.by,
+                                     G.bz, fx.inv_scale);
+        return;
+    }
+    tile_stage_issue(S, T, G, g, pos, vel, warp, lane);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    tile_stage_fix<KMODE>(S, T, G, g, warp, lane);
+    __syncthreads();
+    tile_pairs<RECORD, KMODE>(S, T, G, g, pp, fx, ks, rec, err, tid, warp, lane);
+    __syncthreads();
+    tile_flush(S, T, G, g, fx, frc, warp, lane);
+}
+
+// Persistent variant: gridDim.x resident CTAs walk the tiles t = blockIdx.x + k gridDim.x.
+// While tile t's pairs finish, the first two warps done load tile t + gridDim.x's cell table
+// into the second buffer; its staging copies are issued before tile t's flush (the staging
+// area and the lists are free by then), so their latency overlaps the flush.
+template <bool RECORD, int KMODE>
+__global__ void __launch_bounds__(FT_NTHR, FT_MINB)
+    k_force_tile_p(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
+                   const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
+                   PairRec rec, int *err)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const RoundKeys &ks = rk;
+    const int ntile = tile_count(g);
+    int t = blockIdx.x, b = 0;
+    if (t >= ntile) return;
+    TileGeo G = tile_geo(t, g);
+    if (warp < 2) tile_table(S.tab[0], G, g, start, warp, lane);
+    if (tid == 0) S.done_cnt = 0;
+    __syncthreads();
+    bool fb = tile_overflows(S.tab[0], G);
+    if (!fb) {
+        tile_stage_issue(S, S.tab[0], G, g, pos, vel, warp, lane);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        tile_stage_fix<KMODE>(S, S.tab[0], G, g, warp, lane);
+    }
+    __syncthreads();
+    for (;;) {
+        const int tn = t + gridDim.x;
+        const bool more = tn < ntile;
+        const TileGeo Gn = more ? tile_geo(tn, g) : G;
+        if (fb) {
+            if (tid == 0) atomicAdd(&err[S.tab[b].total > FT_SCAP ? 4 : 5], 1);
+            tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, G.x0, G.y0, G.z0, G.bx, G.by,
+                                         G.bz, fx.inv_scale);
+        } else {
+            tile_pairs<RECORD, KMODE>(S, S.tab[b], G, g, pp, fx, ks, rec, err, tid, warp, lane);
+        }
+        if (more) {
+            int order = 0;
+            if (lane == 0) order = atomicAdd(&S.done_cnt, 1);
+            order = __shfl_sync(0xffffffffu, order, 0);
+            if (order < 2) tile_table(S.tab[b ^ 1], Gn, g, start, order, lane);
+        }
+        __syncthreads(); // pairs of t done, next table ready
+        const bool fbn = more && tile_overflows(S.tab[b ^ 1], Gn);
+        if (more && !fbn) tile_stage_issue(S, S.tab[b ^ 1], Gn, g, pos, vel, warp, lane);
+        if (!fb) tile_flush(S, S.tab[b], G, g, fx, frc, warp, lane);
+        if (tid == 0) S.done_cnt = 0;
+        __syncthreads(); // the sums of t are flushed
+        if (!more) break;
+        if (!fbn) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            tile_stage_fix<KMODE>(S, S.tab[b ^ 1], Gn, g, warp, lane);
+        }
+        __syncthreads();
+        t = tn;
+        G = Gn;
+        b ^= 1;
+        fb = fbn;
     }
 }
 

@@ -16,12 +16,15 @@ pytestmark = pytest.mark.gpu
 FORCE_TOL = 1e-4
 
 
-KERNELS = [0, 1, 2]  # 0: tiled, 1: reference, 2: cell-warp
+KERNELS = [0, 1, 2, "0p"]  # 0: tiled, 1: reference, 2: cell-warp, 0p: tiled as a persistent kernel
 
 
 def _ctx(cfg, seed=None, kernel=0):
     from paper_1911_04712_b200 import capi
     d = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed if seed is None else seed)
+    if kernel == "0p":
+        d.set_option("tile_persistent", 1)
+        kernel = 0
     d.set_option("force_kernel", kernel)
     return d
 
