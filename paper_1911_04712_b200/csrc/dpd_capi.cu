@@ -508,6 +508,7 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         // by the power-of-two scale (exact), so one FFMA per component quantises
         const PairP pp = scaled_pair(c->pp, fx.scale);
         const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp.seed_fold);
+        const dim3 tgrid((g.n[0] + FT_BX - 1) / FT_BX, (g.n[1] + FT_BY - 1) / FT_BY, (g.n[2] + FT_BZ - 1) / FT_BZ);
         const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
                           ((g.n[2] + FT_BZ - 1) / FT_BZ);
         const size_t smem = sizeof(ForceTileSmem);
@@ -519,7 +520,7 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
             k_force_tile_p<R, K><<<std::min(ntile, c->nsm * 3), FT_NTHR, smem, c->stream>>>(                        \
                 c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, c->err.p);                               \
         else                                                                                                        \
-            k_force_tile<R, K><<<ntile, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp,   \
+            k_force_tile<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp,   \
                                                                     fx, rk, rec, c->err.p);                         \
     } while (0)
             if (record) {

@@ -832,7 +832,14 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const RoundKeys &ks = rk; // host-computed round keys of this step (constant bank)
     static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
-    const TileGeo G = tile_geo(blockIdx.x, g);
+    // 3D grid: one CTA per tile, no integer division
+    TileGeo G;
+    G.x0 = blockIdx.x * FT_BX;
+    G.y0 = blockIdx.y * FT_BY;
+    G.z0 = blockIdx.z * FT_BZ;
+    G.bx = min(FT_BX, g.n[0] - G.x0);
+    G.by = min(FT_BY, g.n[1] - G.y0);
+    G.bz = min(FT_BZ, g.n[2] - G.z0);
     TileTab &T = S.tab[0];
     if (warp < 2) tile_table(T, G, g, start, warp, lane);
     __syncthreads();
