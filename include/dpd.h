@@ -80,6 +80,9 @@ int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
  *                  to fp32 summation order).  1 and 2 are single-domain only.
  *   "message_capacity_percent" (distributed contexts) scales the per-direction message
  *                  capacities (default 100; >= 10).
+ *   "tile_persistent" 1 = run the tiled kernel as resident CTAs walking the tiles (the next
+ *                  tile's cell table and staging overlap the current tile's pairs / flush);
+ *                  0 = one CTA per tile (default, measured faster: DESIGN.md §6).
  *   "body_force_mode" 0 = periodic Poiseuille (default), 1 = uniform +f along z.
  *   "dump_delay_us" (after dpd_dump_open) sleep this long before each snapshot write: a
  *                  simulated slow disk for overlap tests (default 0).

@@ -315,7 +315,10 @@ __global__ void __launch_bounds__(256, 8) k_bin(const float4 *__restrict__ pos, 
 // status words carry a launch epoch kept on the device (graph-replay safe).
 // ---------------------------------------------------------------------------------------
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+#ifndef KSCAN_ITEMS
+#define KSCAN_ITEMS 16
+#endif
+constexpr int kScanItems = KSCAN_ITEMS;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 __device__ __forceinline__ unsigned long long scan_pack(unsigned epoch, int flag, int value)
