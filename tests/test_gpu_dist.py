@@ -32,13 +32,16 @@ def destroy(capi, ctxs):
         capi.dpd_destroy(c)
 
 
+@pytest.mark.parametrize("persistent", [0, 1])
 @pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (3, 1, 2)])
-def test_group_prime_forces_match_oracle(grid):
+def test_group_prime_forces_match_oracle(grid, persistent):
     cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
     p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
                          seed=cfg.seed)
     pos0, vel0 = workloads.make_config(cfg)
     capi, ctxs = make_group(cfg, grid)
+    for c in ctxs:  # the tiled kernel with halo rings, one CTA per tile or resident CTAs
+        capi.dpd_set_option(c, "tile_persistent", persistent)
     try:
         ids0 = np.arange(pos0.shape[0], dtype=np.int32)
         for c in ctxs:  # every member receives the global set and keeps its own share
