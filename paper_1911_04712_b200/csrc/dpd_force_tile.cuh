@@ -27,7 +27,7 @@
 #define FT_CPASYNC "cp.async.cg.shared.global" // staging copies bypass L1 (.ca measured 457 vs .cg 452 us)
 #endif
 #ifndef FT_SWEEP_TAIL
-#define FT_SWEEP_TAIL 0 // 0: 2-wide + 1-wide tails, 1: one masked 4-block
+#define FT_SWEEP_TAIL 2 // 0: odd prologue + 2/1-wide tails, 1: masked 4-block tail, 2: 4-aligned LDS.128 blocks, masked ends (433.0 vs 434.0 us)
 #endif
 #ifndef FT_SWEEP_UNROLL
 #define FT_SWEEP_UNROLL 1 // unroll of the 4-candidate sweep loop (measured: 1 -> 457, 2 -> 468, 4 -> 477 us)
@@ -111,6 +111,9 @@ __device__ __forceinline__ int ext_coord(int c, int n, int split)
 
 static_assert(sizeof(unsigned short) * FT_NTHR * FT_LSTRIDE >= sizeof(float4) * FT_SCAP,
               "the list area doubles as the position landing buffer");
+static_assert(FT_SWEEP_TAIL != 2 || (offsetof(ForceTileSmem, sx) % 16 == 0 && offsetof(ForceTileSmem, sy) % 16 == 0 &&
+                                     offsetof(ForceTileSmem, sz) % 16 == 0),
+              "LDS.128 candidate quads");
 static_assert(offsetof(ForceTileSmem, lst) % 16 == 0 && offsetof(ForceTileSmem, sx) % 8 == 0 &&
                   offsetof(ForceTileSmem, sy) % 8 == 0 && offsetof(ForceTileSmem, sz) % 8 == 0,
               "cp.async / packed-pair alignment");
@@ -212,10 +215,61 @@ __device__ __forceinline__ void append_if_lt(unsigned &lptr, float r2, float rc2
                  : "memory");
 }
 
+// Append j if r2 < rc2 and lo <= j < hi (the masked end blocks of the aligned sweep).
+__device__ __forceinline__ void append_if_in(unsigned &lptr, float r2, float rc2, unsigned j, int lo, int hi)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tsetp.ge.and.s32 p, %3, %4, p;\n\t"
+                 "setp.lt.and.s32 p, %3, %5, p;\n\t@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
+                 : "+r"(lptr)
+                 : "f"(r2), "f"(rc2), "r"(j), "r"(lo), "r"(hi)
+                 : "memory");
+}
+
+// Four candidates j..j+3 (j % 4 == 0): one LDS.128 per coordinate, packed r2.
+__device__ __forceinline__ void r2_quad(const ForceTileSmem &S, int j, unsigned long long PX, unsigned long long PY,
+                                        unsigned long long PZ, float &ra, float &rb, float &rc, float &rd)
+{
+    const ulonglong2 X = *reinterpret_cast<const ulonglong2 *>(&S.sx[j]);
+    const ulonglong2 Y = *reinterpret_cast<const ulonglong2 *>(&S.sy[j]);
+    const ulonglong2 Z = *reinterpret_cast<const ulonglong2 *>(&S.sz[j]);
+    r2_pair(X.x, Y.x, Z.x, PX, PY, PZ, ra, rb);
+    r2_pair(X.y, Y.y, Z.y, PX, PY, PZ, rc, rd);
+}
+
 // Sweep of one contiguous smem segment [lo, hi): append every in-cutoff j.
 __device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, int lo, int hi, float px, float py,
                                       float pz, float rc2)
 {
+#if FT_SWEEP_TAIL == 2
+    // 4-aligned blocks (LDS.128 per coordinate); the first and last blocks masked to [lo, hi)
+    // (reads outside the segment stay inside the shared struct)
+    const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
+    int j = lo & ~3;
+    float ra, rb, rc, rd;
+    if (j < hi) {
+        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
+        append_if_in(lptr, ra, rc2, (unsigned)j, lo, hi);
+        append_if_in(lptr, rb, rc2, (unsigned)(j + 1), lo, hi);
+        append_if_in(lptr, rc, rc2, (unsigned)(j + 2), lo, hi);
+        append_if_in(lptr, rd, rc2, (unsigned)(j + 3), lo, hi);
+        j += 4;
+    }
+#pragma unroll kSweepUnroll
+    for (; j + 3 < hi; j += 4) {
+        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
+        append_if(lptr, ra, rc2, (unsigned)j);
+        append_if(lptr, rb, rc2, (unsigned)(j + 1));
+        append_if(lptr, rc, rc2, (unsigned)(j + 2));
+        append_if(lptr, rd, rc2, (unsigned)(j + 3));
+    }
+    if (j < hi) {
+        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
+        append_if(lptr, ra, rc2, (unsigned)j);
+        append_if_lt(lptr, rb, rc2, (unsigned)(j + 1), hi);
+        append_if_lt(lptr, rc, rc2, (unsigned)(j + 2), hi);
+        append_if_lt(lptr, rd, rc2, (unsigned)(j + 3), hi);
+    }
+#else
     int j = lo;
     if ((j & 1) && j < hi) {
         append_if(lptr, r2_one(S, j, px, py, pz), rc2, (unsigned)j);
@@ -253,6 +307,7 @@ __device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, in
         j += 2;
     }
     if (j < hi) append_if(lptr, r2_one(S, j, px, py, pz), rc2, (unsigned)j);
+#endif
 #endif
 }
 
