@@ -1,52 +1,34 @@
 // dpd_force_tile.cuh -- production pair-force sweep for sm_100a.
 //
-// One CTA per tile of BX x BY x BZ home cells (cell lists, symmetric forces):
-//   1. stage   : the tile's forward half-stencil region, (BX+2) x (BY+2) x (BZ+1) cells,
-//                is copied row by row (contiguous global ranges) into shared memory, with
-//                periodic images pre-shifted into the tile frame (AoS float4 + an SoA copy
-//                of x, y, z for the packed sweep);
-//   2. sweep   : thread h owns home particle h and sweeps its 5 contiguous smem segments
-//                (own cell after i + next cell, the y+1 row, three z+1 rows) two candidates
-//                at a time with packed fp32x2 arithmetic (FADD2/FFMA2), appending in-cutoff
-//                j to the particle's list -- one predicated store + add per hit;
-//   3. pairs   : the CTA-wide concatenation of all lists is cut into NTHR contiguous chunks
-//                (perfect load balance across warps); a chunk spans one or two owners, so the
-//                i-side sum stays in registers;
-//   4. accumulate: f is quantised once to 32-bit fixed point and added with native
-//                shared-memory integer atomics (+q on i, -q on j): exact Newton-3,
-//                order-independent sums;
-//   5. flush   : every staged particle's sum is converted back to fp32 and added to the
+// One CTA of 9 warps per tile of BX x BY x BZ home cells (cell lists, symmetric
+// forces), 3 tiles resident per SM (74 KB shared memory, 72 registers); launched on a 3D grid,
+// one CTA per tile (or, option tile_persistent, as resident CTAs walking the tiles):
+//   1. table   : one warp loads the staged cell table of the forward half-stencil region,
+//                (BX+2) x (BY+2) x (BZ+1) cells, straight from the cell starts and scans it;
+//                another warp scans the home rows;
+//   2. stage   : every staged row (<= 3 contiguous global ranges) is copied with cp.async.cg,
+//                then shifted to the periodic image in the tile frame and split into SoA
+//                x, y, z; the particle id rides in the staged velocity's w word;
+//   3. sweep   : one home particle per lane sweeps its 5 contiguous smem segments (own cell
+//                after i + next cell, the y+1 row, three z+1 rows; row ends beyond r_c
+//                pruned) in 4-aligned blocks -- one LDS.128 per coordinate, packed fp32x2
+//                distance math (FADD2/FFMA2), one predicated 16-bit store + add per hit;
+//   4. pairs   : the warp's lists are concatenated and cut into 32 contiguous lane chunks,
+//                each walked by two cursors (two Philox/Box-Muller chains in flight); the
+//                i-side sum stays in registers until the owner changes;
+//   5. accumulate: a, gamma, sigma are pre-scaled by the power-of-two fixed-point scale, so
+//                one FFMA quantises each force component; native shared-memory integer
+//                atomics (+q on i, -q on j): exact Newton-3, order-independent sums;
+//   6. flush   : every staged particle's sum is converted back to fp32 and added to the
 //                global force array with one vector reduction (REDG.F32x4).
 // Tiles whose particle counts exceed the shared-memory capacities (never seen at rho = 8,
 // > 9 sigma) are evaluated by a direct global-memory fallback with the same pair function.
+// DESIGN.md §6 records the measured history of every choice.
 #pragma once
 
 #include "dpd_kernels.cuh"
 
-#ifndef FT_CPASYNC
-#define FT_CPASYNC "cp.async.cg.shared.global" // staging copies bypass L1 (.ca measured 457 vs .cg 452 us)
-#endif
-#ifndef FT_SWEEP_TAIL
-#define FT_SWEEP_TAIL 2 // 0: odd prologue + 2/1-wide tails, 1: masked 4-block tail, 2: 4-aligned LDS.128 blocks, masked ends (433.0 vs 434.0 us)
-#endif
-#ifndef FT_SWEEP_UNROLL
-#define FT_SWEEP_UNROLL 1 // unroll of the 4-candidate sweep loop (measured: 1 -> 457, 2 -> 468, 4 -> 477 us)
-#endif
-
 namespace dpd {
-
-constexpr int kSweepUnroll = FT_SWEEP_UNROLL;
-#ifndef FT_SEG_UNROLL
-#define FT_SEG_UNROLL 5 // unroll of the 5-segment loop of the sweep (measured: 1 -> 457, 5 -> 449 us)
-#endif
-constexpr int kSegUnroll = FT_SEG_UNROLL;
-#ifndef FT_STAGE_UNROLL
-#define FT_STAGE_UNROLL 1 // unroll of the per-lane staging copy / fix loops
-#endif
-constexpr int kStageUnroll = FT_STAGE_UNROLL;
-#ifndef FT_EXPECT
-#define FT_EXPECT 0 // owner switches of the pair cursors marked unlikely
-#endif
 
 constexpr int FT_BX = 4, FT_BY = 4, FT_BZ = 2;
 constexpr int FT_SX = FT_BX + 2, FT_SY = FT_BY + 2, FT_SZ = FT_BZ + 1;
@@ -111,8 +93,8 @@ __device__ __forceinline__ int ext_coord(int c, int n, int split)
 
 static_assert(sizeof(unsigned short) * FT_NTHR * FT_LSTRIDE >= sizeof(float4) * FT_SCAP,
               "the list area doubles as the position landing buffer");
-static_assert(FT_SWEEP_TAIL != 2 || (offsetof(ForceTileSmem, sx) % 16 == 0 && offsetof(ForceTileSmem, sy) % 16 == 0 &&
-                                     offsetof(ForceTileSmem, sz) % 16 == 0),
+static_assert(offsetof(ForceTileSmem, sx) % 16 == 0 && offsetof(ForceTileSmem, sy) % 16 == 0 &&
+                  offsetof(ForceTileSmem, sz) % 16 == 0,
               "LDS.128 candidate quads");
 static_assert(offsetof(ForceTileSmem, lst) % 16 == 0 && offsetof(ForceTileSmem, sx) % 8 == 0 &&
                   offsetof(ForceTileSmem, sy) % 8 == 0 && offsetof(ForceTileSmem, sz) % 8 == 0,
@@ -240,7 +222,6 @@ __device__ __forceinline__ void r2_quad(const ForceTileSmem &S, int j, unsigned 
 __device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, int lo, int hi, float px, float py,
                                       float pz, float rc2)
 {
-#if FT_SWEEP_TAIL == 2
     // 4-aligned blocks (LDS.128 per coordinate); the first and last blocks masked to [lo, hi)
     // (reads outside the segment stay inside the shared struct)
     const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
@@ -254,7 +235,7 @@ __device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, in
         append_if_in(lptr, rd, rc2, (unsigned)(j + 3), lo, hi);
         j += 4;
     }
-#pragma unroll kSweepUnroll
+#pragma unroll 1 // measured: no unroll 457, x2 468, x4 477 us (the remainder cascade runs at 9-11 lanes)
     for (; j + 3 < hi; j += 4) {
         r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
         append_if(lptr, ra, rc2, (unsigned)j);
@@ -269,53 +250,14 @@ __device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, in
         append_if_lt(lptr, rc, rc2, (unsigned)(j + 2), hi);
         append_if_lt(lptr, rd, rc2, (unsigned)(j + 3), hi);
     }
-#else
-    int j = lo;
-    if ((j & 1) && j < hi) {
-        append_if(lptr, r2_one(S, j, px, py, pz), rc2, (unsigned)j);
-        ++j;
-    }
-    const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
-    // four candidates per iteration: two independent packed chains in flight (ILP)
-#pragma unroll kSweepUnroll
-    for (; j + 3 < hi; j += 4) {
-        float ra, rb, rc, rd;
-        r2_pair(ld_f2(&S.sx[j]), ld_f2(&S.sy[j]), ld_f2(&S.sz[j]), PX, PY, PZ, ra, rb);
-        r2_pair(ld_f2(&S.sx[j + 2]), ld_f2(&S.sy[j + 2]), ld_f2(&S.sz[j + 2]), PX, PY, PZ, rc, rd);
-        append_if(lptr, ra, rc2, (unsigned)j);
-        append_if(lptr, rb, rc2, (unsigned)(j + 1));
-        append_if(lptr, rc, rc2, (unsigned)(j + 2));
-        append_if(lptr, rd, rc2, (unsigned)(j + 3));
-    }
-#if FT_SWEEP_TAIL == 1
-    // remaining 1..3 candidates: one masked 4-block (reads past hi stay inside the struct)
-    if (j < hi) {
-        float ra, rb, rc, rd;
-        r2_pair(ld_f2(&S.sx[j]), ld_f2(&S.sy[j]), ld_f2(&S.sz[j]), PX, PY, PZ, ra, rb);
-        r2_pair(ld_f2(&S.sx[j + 2]), ld_f2(&S.sy[j + 2]), ld_f2(&S.sz[j + 2]), PX, PY, PZ, rc, rd);
-        append_if(lptr, ra, rc2, (unsigned)j);
-        append_if_lt(lptr, rb, rc2, (unsigned)(j + 1), hi);
-        append_if_lt(lptr, rc, rc2, (unsigned)(j + 2), hi);
-        append_if_lt(lptr, rd, rc2, (unsigned)(j + 3), hi);
-    }
-#else
-    if (j + 1 < hi) {
-        float ra, rb;
-        r2_pair(ld_f2(&S.sx[j]), ld_f2(&S.sy[j]), ld_f2(&S.sz[j]), PX, PY, PZ, ra, rb);
-        append_if(lptr, ra, rc2, (unsigned)j);
-        append_if(lptr, rb, rc2, (unsigned)(j + 1));
-        j += 2;
-    }
-    if (j < hi) append_if(lptr, r2_one(S, j, px, py, pz), rc2, (unsigned)j);
-#endif
-#endif
 }
 
 // Asynchronous copy (LDGSTS, no register round trip) of global particles [g0, g0 + len)
 // to smem [s0, s0 + len): every load of the tile is in flight before any is waited for.
 __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 {
-    asm volatile(FT_CPASYNC " [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+    // .cg: the staged rows bypass L1 (measured .ca 457 vs .cg 452 us)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                  "l"(src)
                  : "memory");
 }
@@ -323,7 +265,6 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__restrict__ pos,
                                            const float4 *__restrict__ vel, int g0, int s0, int len, int lane)
 {
-#pragma unroll kStageUnroll
     for (int k = lane; k < len; k += 32) {
         cp_async16(reinterpret_cast<float4 *>(S.lst) + s0 + k, &pos[g0 + k]);
         cp_async16(&S.sv[s0 + k], &vel[g0 + k]);
@@ -335,7 +276,6 @@ __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__res
 template <int KMODE>
 __device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, float sx, float sy, float sz, int lane)
 {
-#pragma unroll kStageUnroll
     for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
         const float4 p = reinterpret_cast<const float4 *>(S.lst)[s];
@@ -474,11 +414,7 @@ __device__ __forceinline__ void cursor_flush(PairCursor &c, ForceTileSmem &S)
 // Entry t of the list (the partner j); moves to the next owner first when t crosses it.
 __device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
 {
-#if FT_EXPECT
-    if (__builtin_expect(c.t >= c.enext, 0)) { // next owner (never empty)
-#else
     if (c.t >= c.enext) { // next owner (never empty)
-#endif
         cursor_flush(c, S);
         ++c.o;
         cursor_load(c, S);
@@ -742,7 +678,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             const float dzr = fmaxf(hz - oz - fx.slack, 0.0f);
             unsigned lptr = lbase;
             bool full = false;
-#pragma unroll kSegUnroll
+#pragma unroll // all five segments (measured 457 -> 449 us against a rolled loop)
             for (int k = 0; k < 5; ++k) {
                 // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
                 const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
