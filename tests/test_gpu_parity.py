@@ -320,10 +320,11 @@ def test_per_step_parity_ragged_boxes(box, rho, kernel):
             d.step(1)
 
 
-@pytest.mark.parametrize("name", ["pois96", "weak128"])
+@pytest.mark.parametrize("name", ["pois96", "weak128", "strong256"])
 def test_full_size_sampled_parity_other_configs(name):
-    """BASELINE configs 3 and 4 at full size (7.1 M / 16.8 M particles) in bench's launch
-    configuration: sampled all-j sums against the oracle, cell counts bit-exact, sum F = 0."""
+    """BASELINE configs 3, 4 and 5 at full size (7.1 M / 16.8 M / 134 M particles, the last
+    one whole on one GPU) in bench's launch configuration: sampled all-j sums against the
+    oracle, cell counts bit-exact, sum F = 0."""
     cfg = workloads.CONFIGS[name]
     p = _params(cfg)
     eps = boundary_eps(cfg.box)
