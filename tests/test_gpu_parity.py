@@ -244,6 +244,35 @@ def test_temperature_rho8():
     assert abs(T - cfg.kT) < 0.01 * cfg.kT, T
 
 
+@pytest.mark.parametrize("a", [50.0, 10.0])
+def test_groot_warren_pressure_rho8(a):
+    """Structure of the GPU-sampled ensemble: p = rho T + W / (3V) with the conservative virial
+    W = sum a w(r) r evaluated by the oracle on the GPU's configurations (C-2 item 6) against
+    the Groot-Warren EOS p = rho kT + 0.101 a rho^2 within 2 % at rho = 8 (C-15; survey
+    measurement +0.5 % / -0.6 % for a = 50 / 10).  8^3 box (4096 particles), Table-2 gamma and
+    dt (P:489), k = 1/2."""
+    cfg = workloads.with_box(workloads.CONFIGS["eq64"], (8.0, 8.0, 8.0))
+    d_ = cfg.as_dict()
+    d_["a"] = a
+    cfg = workloads.Config(**d_)
+    p = _params(cfg)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    d.step(1000)
+    T, W = [], []
+    for _ in range(60):
+        d.step(20)
+        x, v = d.get_particles()
+        T.append(oracle.temperature(v))
+        W.append(oracle.virial(p, x))
+    V = float(np.prod(cfg.box))
+    pr = cfg.rho * np.mean(T) + np.mean(W) / (3.0 * V)
+    gw = cfg.rho * cfg.kT + 0.101 * a * cfg.rho ** 2
+    assert abs(np.mean(T) - cfg.kT) < 0.015 * cfg.kT, np.mean(T)
+    assert abs(pr - gw) / gw < 0.02, (pr, gw)
+
+
 def test_resume_reproduces_rng_words():
     # checkpoint/resume (C-20): set_particles_ex(ids, step0) continues the same RNG stream
     from paper_1911_04712_b200 import capi
