@@ -163,6 +163,7 @@ struct dpd_ctx {
     double cap_factor = 1.0;
     bool msgs_ready = false;
     DevBuf<int> rank_in, gcount, gstart, grank;
+    DevBuf<int> blist; // [0]: count, then the local indices of the boundary-layer particles (row a9)
     DevBuf<float4> gpos, gvel;
     DevBuf<unsigned long long> gscan_state;
     int64_t gcap = 0;
@@ -430,10 +431,14 @@ int phase_ghost_pack(dpd_ctx *c)
 {
     const Geom g = c->geom;
     const Msgs gs = c->gh.ms;
+    CUDA_TRY(c, c->blist.reserve((size_t)c->n_cap + 1));
+    CUDA_TRY(c, cudaMemsetAsync(c->blist.p, 0, sizeof(int), c->stream));
     TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(gs); }));
+    const int ncell_in = g.n[0] * g.n[1] * g.n[2];
     return launch(c, KID_GHOST_PACK, [&] {
-        k_ghost_pack<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[c->cur].p, c->vel[c->cur].p, count_ptr(c), g,
-                                                                 gs, c->err.p);
+        k_ghost_pack_cells<<<nblk(ncell_in, 256), 256, 0, c->stream>>>(c->pos[c->cur].p, c->vel[c->cur].p,
+                                                                        c->start[c->scur].p, g, gs, c->blist.p,
+                                                                        c->err.p);
     });
 }
 
@@ -589,13 +594,18 @@ int phase_halo(dpd_ctx *c, int64_t step)
     const PairP pp = c->pp;
     const int b = c->cur;
     return launch(c, KID_HALO, [&] {
-        const unsigned nb = nblk(c->n_cap, 128);
+        // grid-stride over the boundary list (its length lives on the device)
+        const unsigned nb = (unsigned)std::min<int64_t>(nblk(c->n_cap, 128), (int64_t)c->nsm * 16);
+#define DPD_HALO(K)                                                                                                 \
+    k_force_halo_list<K><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, c->blist.p, c->gpos.p,   \
+                                                    c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi)
         switch (c->kmode) {
-        case 0: k_force_halo<0><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
-        case 1: k_force_halo<1><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
-        case 2: k_force_halo<2><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
-        default: k_force_halo<3><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, count_ptr(c), c->gpos.p, c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi); break;
+        case 0: DPD_HALO(0); break;
+        case 1: DPD_HALO(1); break;
+        case 2: DPD_HALO(2); break;
+        default: DPD_HALO(3); break;
         }
+#undef DPD_HALO
     });
 }
 
@@ -1215,6 +1225,7 @@ void dpd_destroy(dpd_ctx *c)
     c->gh.recv.release();
     c->rank_in.release();
     c->gcount.release();
+    c->blist.release();
     c->gstart.release();
     c->grank.release();
     c->gpos.release();
