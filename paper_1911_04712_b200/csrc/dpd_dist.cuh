@@ -261,54 +261,94 @@ __global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restri
 // Local particle i in a boundary cell sums f_ij over the ghosts j of its halo neighbour
 // cells; the peer rank computes the exact negation for its own copy (global ids key the
 // RNG, C-19).  Runs after the interior pass on the same stream: plain read-modify-write.
+// Halo neighbour cell d (0..26 = dir_index) of interior cell ci: extended-grid index and the
+// periodic shift of its ghosts; -1 if the cell is not in the halo ring.
+__device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, float sh[3])
+{
+    const int dd[3] = {d % 3 - 1, (d / 3) % 3 - 1, d / 9 - 1};
+    int e[3];
+    bool halo = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int jc = ci[k] + dd[k];
+        sh[k] = 0.0f;
+        if (g.split[k]) {
+            halo |= (jc < 0 || jc >= g.n[k]);
+            e[k] = jc + 1;
+        } else {
+            if (jc < 0) {
+                jc += g.n[k];
+                sh[k] = -g.L[k];
+            } else if (jc >= g.n[k]) {
+                jc -= g.n[k];
+                sh[k] = g.L[k];
+            }
+            e[k] = jc;
+        }
+    }
+    return halo ? e[0] + g.ext[0] * (e[1] + g.ext[1] * e[2]) : -1;
+}
+
+// One local-ghost pair (one-sided: the force on local i only).
+template <int KMODE>
+__device__ __forceinline__ void halo_pair(const float4 &pi, const float4 &vi, const float4 &pj, const float4 &vj,
+                                          const float sh[3], const PairP &pp, uint32_t ks, float &Fx, float &Fy,
+                                          float &Fz)
+{
+    const float rx = pi.x - (pj.x + sh[0]), ry = pi.y - (pj.y + sh[1]), rz = pi.z - (pj.z + sh[2]);
+    const float r2 = rx * rx + ry * ry + rz * rz;
+    const float dv = rx * (vi.x - vj.x) + ry * (vi.y - vj.y) + rz * (vi.z - vj.z);
+    const float s = pair_scalar<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(pi.w), (uint32_t)__float_as_int(pj.w), ks,
+                                       vi.w, vj.w);
+    Fx += s * rx;
+    Fy += s * ry;
+    Fz += s * rz;
+}
+
+constexpr int kHaloThreads = 128;
+constexpr int kHaloCap = 24; // hits kept per boundary particle before evaluating in place (mean ~6-12)
+
 // Halo forces of local particle i: all ghosts j of its halo neighbour cells (one-sided).
+// Two passes: the distance sweep collects the hits (ghost index | neighbour code << 27) in
+// the thread's shared-memory list, then the pair bodies run back to back -- the heavy pair
+// body is not executed for every candidate a neighbour lane hits.
 template <int KMODE>
 __device__ __forceinline__ void halo_particle(int i, const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                               float4 *__restrict__ frc, const float4 *__restrict__ gpos,
                                               const float4 *__restrict__ gvel, const int *__restrict__ gstart,
-                                              const Geom &g, const PairP &pp, uint32_t ks)
+                                              const Geom &g, const PairP &pp, uint32_t ks, unsigned *hl)
 {
     const float4 pi = pos[i];
     const int ci[3] = {cell_coord(pi.x, g.inv_h[0], g.n[0]), cell_coord(pi.y, g.inv_h[1], g.n[1]),
                        cell_coord(pi.z, g.inv_h[2], g.n[2])};
     const float4 vi = vel[i];
-    const uint32_t idi = (uint32_t)__float_as_int(pi.w);
     float Fx = 0.f, Fy = 0.f, Fz = 0.f;
-    for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int dd[3] = {dx, dy, dz};
-                int e[3];
-                float sh[3] = {0.f, 0.f, 0.f};
-                bool halo = false;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    int jc = ci[k] + dd[k];
-                    if (g.split[k]) {
-                        halo |= (jc < 0 || jc >= g.n[k]);
-                        e[k] = jc + 1;
-                    } else {
-                        if (jc < 0) { jc += g.n[k]; sh[k] = -g.L[k]; }
-                        else if (jc >= g.n[k]) { jc -= g.n[k]; sh[k] = g.L[k]; }
-                        e[k] = jc;
-                    }
-                }
-                if (!halo) continue;
-                const int c = e[0] + g.ext[0] * (e[1] + g.ext[1] * e[2]);
-                for (int j = gstart[c]; j < gstart[c + 1]; ++j) {
-                    const float4 pj = gpos[j];
-                    const float rx = pi.x - (pj.x + sh[0]), ry = pi.y - (pj.y + sh[1]), rz = pi.z - (pj.z + sh[2]);
-                    const float r2 = rx * rx + ry * ry + rz * rz;
-                    if (r2 < pp.rc2 && r2 > 0.0f) {
-                        const float4 vj = gvel[j];
-                        const float dv = rx * (vi.x - vj.x) + ry * (vi.y - vj.y) + rz * (vi.z - vj.z);
-                        const float s = pair_scalar<KMODE>(pp, r2, dv, idi, (uint32_t)__float_as_int(pj.w), ks, vi.w, vj.w);
-                        Fx += s * rx;
-                        Fy += s * ry;
-                        Fz += s * rz;
-                    }
+    int nh = 0;
+    for (int d = 0; d < 27; ++d) {
+        float sh[3];
+        const int c = halo_cell(g, ci, d, sh);
+        if (c < 0) continue;
+        for (int j = gstart[c]; j < gstart[c + 1]; ++j) {
+            const float4 pj = gpos[j];
+            const float rx = pi.x - (pj.x + sh[0]), ry = pi.y - (pj.y + sh[1]), rz = pi.z - (pj.z + sh[2]);
+            const float r2 = rx * rx + ry * ry + rz * rz;
+            if (r2 < pp.rc2 && r2 > 0.0f) {
+                if (nh < kHaloCap) {
+                    hl[nh * kHaloThreads] = (unsigned)j | ((unsigned)d << 27);
+                    ++nh;
+                } else {
+                    halo_pair<KMODE>(pi, vi, pj, gvel[j], sh, pp, ks, Fx, Fy, Fz);
                 }
             }
+        }
+    }
+    for (int k = 0; k < nh; ++k) {
+        const unsigned e = hl[k * kHaloThreads];
+        const int j = (int)(e & 0x07FFFFFFu);
+        float sh[3];
+        halo_cell(g, ci, (int)(e >> 27), sh);
+        halo_pair<KMODE>(pi, vi, gpos[j], gvel[j], sh, pp, ks, Fx, Fy, Fz);
+    }
     float4 f = frc[i];
     f.x += Fx;
     f.y += Fy;
@@ -317,7 +357,7 @@ __device__ __forceinline__ void halo_particle(int i, const float4 *__restrict__ 
 }
 
 template <int KMODE>
-__global__ void __launch_bounds__(128) k_force_halo(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+__global__ void __launch_bounds__(kHaloThreads) k_force_halo(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                                     float4 *__restrict__ frc, const int *__restrict__ n_ptr,
                                                     const float4 *__restrict__ gpos, const float4 *__restrict__ gvel,
                                                     const int *__restrict__ gstart, Geom g, PairP pp,
@@ -331,24 +371,27 @@ __global__ void __launch_bounds__(128) k_force_halo(const float4 *__restrict__ p
     bool boundary = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) boundary |= g.split[k] && (ci[k] == 0 || ci[k] == g.n[k] - 1);
+    __shared__ unsigned hl[kHaloThreads * kHaloCap];
     if (!boundary) return;
-    halo_particle<KMODE>(i, pos, vel, frc, gpos, gvel, gstart, g, pp, step_key(s_lo, s_hi, pp.seed_fold));
+    halo_particle<KMODE>(i, pos, vel, frc, gpos, gvel, gstart, g, pp, step_key(s_lo, s_hi, pp.seed_fold),
+                         hl + threadIdx.x);
 }
 
 // The same over the boundary list of k_ghost_pack_cells (blist[0] entries): every thread
 // busy, no pass over the interior particles.
 template <int KMODE>
-__global__ void __launch_bounds__(128) k_force_halo_list(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
+__global__ void __launch_bounds__(kHaloThreads) k_force_halo_list(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                                          float4 *__restrict__ frc, const int *__restrict__ blist,
                                                          const float4 *__restrict__ gpos,
                                                          const float4 *__restrict__ gvel,
                                                          const int *__restrict__ gstart, Geom g, PairP pp,
                                                          uint32_t s_lo, uint32_t s_hi)
 {
+    __shared__ unsigned hl[kHaloThreads * kHaloCap];
     const int nb = blist[0];
     const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x)
-        halo_particle<KMODE>(blist[1 + t], pos, vel, frc, gpos, gvel, gstart, g, pp, ks);
+        halo_particle<KMODE>(blist[1 + t], pos, vel, frc, gpos, gvel, gstart, g, pp, ks, hl + threadIdx.x);
 }
 
 } // namespace dpd
