@@ -431,7 +431,7 @@ int phase_ghost_pack(dpd_ctx *c)
 {
     const Geom g = c->geom;
     const Msgs gs = c->gh.ms;
-    CUDA_TRY(c, c->blist.reserve((size_t)c->n_cap + 1));
+    CUDA_TRY(c, c->blist.reserve((size_t)g.ncell + 1));
     CUDA_TRY(c, cudaMemsetAsync(c->blist.p, 0, sizeof(int), c->stream));
     TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(gs); }));
     const int ncell_in = g.n[0] * g.n[1] * g.n[2];
@@ -595,10 +595,12 @@ int phase_halo(dpd_ctx *c, int64_t step)
     const int b = c->cur;
     return launch(c, KID_HALO, [&] {
         // grid-stride over the boundary list (its length lives on the device)
-        const unsigned nb = (unsigned)std::min<int64_t>(nblk(c->n_cap, 128), (int64_t)c->nsm * 16);
+        const unsigned nbh = (unsigned)c->nsm * 16; // grid-stride over the boundary cells (count on device)
 #define DPD_HALO(K)                                                                                                 \
-    k_force_halo_list<K><<<nb, 128, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, c->blist.p, c->gpos.p,   \
-                                                    c->gvel.p, c->gstart.p, g, pp, s_lo, s_hi)
+    k_force_halo_cells<K><<<nbh, 32 * kHcWarps, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, c->blist.p,  \
+                                                                c->start[c->scur].p, c->gpos.p, c->gvel.p,          \
+                                                                c->gstart.p, g, pp, c->fix.scale, c->fix.inv_scale, \
+                                                                s_lo, s_hi)
         switch (c->kmode) {
         case 0: DPD_HALO(0); break;
         case 1: DPD_HALO(1); break;
@@ -708,6 +710,9 @@ int setup_messages(dpd_ctx *c, double rho)
     int64_t gtot = 0;
     for (int d = 0; d < 27; ++d) gtot += c->gh.ms.cap[d];
     c->gcap = gtot;
+    if (gtot >= ((int64_t)1 << 22))
+        return fail(c, DPD_ERR_CAPACITY, "ghost capacity %lld exceeds the halo kernel's 2^22 ghost index range",
+                    (long long)gtot);
     CUDA_TRY(c, c->gpos.reserve((size_t)std::max<int64_t>(gtot, 1)));
     CUDA_TRY(c, c->gvel.reserve((size_t)std::max<int64_t>(gtot, 1)));
     c->msgs_ready = true;

@@ -83,54 +83,6 @@ __global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxc
     frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 }
 
-// ---- row a7: ghost identify + pack ------------------------------------------------------
-// A particle in the first (last) interior cell layer of a split dimension goes to the
-// neighbour below (above); edge and corner cells go to every combination (up to 7 messages).
-__global__ void __launch_bounds__(256) k_ghost_pack(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                                                    const int *__restrict__ n_ptr, Geom g, Msgs gs, int *err)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int n = *n_ptr;
-    float4 p = make_float4(0.f, 0.f, 0.f, 0.f), v = p;
-    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    if (i < n) {
-        p = pos[i];
-        v = vel[i];
-        const float xs[3] = {p.x, p.y, p.z};
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (!g.split[k]) continue;
-            const int ic = cell_coord(xs[k], g.inv_h[k], g.n[k]);
-            lo[k] = ic == 0;
-            hi[k] = ic == g.n[k] - 1;
-        }
-    }
-    const int lane = threadIdx.x & 31;
-    for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int d = dir_index(dx, dy, dz);
-                if (d == 13 || gs.cap[d] == 0) continue; // uniform
-                const bool want = i < n && (dx == 0 || (dx < 0 ? lo[0] : hi[0])) &&
-                                  (dy == 0 || (dy < 0 ? lo[1] : hi[1])) && (dz == 0 || (dz < 0 ? lo[2] : hi[2]));
-                const unsigned m = __ballot_sync(0xffffffffu, want);
-                if (!m) continue;
-                int base = 0;
-                const int leader = __ffs(m) - 1;
-                if (lane == leader) base = atomicAdd(msg_count(gs, d), __popc(m));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (want) {
-                    const int slot = base + __popc(m & lanemask_lt());
-                    if (slot < gs.cap[d]) {
-                        float4 *q = msg_data(gs, d) + 2 * slot;
-                        q[0] = make_float4(p.x - dx * g.L[0], p.y - dy * g.L[1], p.z - dz * g.L[2], p.w);
-                        q[1] = v;
-                    } else {
-                        raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
-                    }
-                }
-            }
-}
 
 // ---- rows a8/a9: received ghosts -> halo cells (count, scan, scatter) ------------------
 __global__ void __launch_bounds__(256) k_ghost_bin(Msgs rec, Geom g, int maxcap, int *__restrict__ gcount,
@@ -164,13 +116,14 @@ __global__ void __launch_bounds__(256) k_ghost_scatter(Msgs rec, Geom g, int max
     gvel[dst] = msg_data(rec, d)[2 * k + 1];
 }
 
-// ---- row a7 (cell-driven): one thread per interior cell; only the cells of the boundary
-// layers of split dimensions do work.  A boundary cell's particles (contiguous in the sorted
-// arrays) are written to every direction its position calls for (face / edge / corner) with
-// one warp-aggregated slot reservation per direction, and appended to the boundary list
-// blist[1..blist[0]] that drives the halo force (row a9).  Same messages as k_ghost_pack
-// (a multiset: the order inside a message is irrelevant to the receiver's binning), ~5 % of
-// the work at 128^3 per rank.
+// ---- row a7: ghost identify + pack, one thread per interior cell ---------------------------
+// Only the cells of the boundary layers of split dimensions do work (~5 % at 128^3 per
+// rank).  A boundary cell's particles (contiguous in the sorted arrays) are written to every
+// direction its position calls for (face / edge / corner: a corner cell's particles go to 7
+// messages), shifted by -D L_sub into the receiver's frame, with one warp-aggregated slot
+// reservation per direction; the cell itself is appended to the boundary-cell list
+// blist[1..blist[0]] that drives the halo force (row a9).  The order inside a message is
+// irrelevant: the receiver bins the ghosts into its halo ring.
 __global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restrict__ pos,
                                                           const float4 *__restrict__ vel,
                                                           const int *__restrict__ start, Geom g, Msgs gs,
@@ -206,21 +159,19 @@ __global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restri
                     }
         }
     }
-    // boundary list
+    // boundary-cell list (extended-grid index of every non-empty boundary cell)
     {
-        const int v = border ? cnt : 0;
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
-        if (tot) {
+        const bool has = border && cnt > 0;
+        const unsigned bm = __ballot_sync(0xffffffffu, has);
+        if (bm) {
             int base = 0;
-            if (lane == 31) base = atomicAdd(&blist[0], tot);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            for (int k = 0; k < v; ++k) blist[1 + base + incl - v + k] = s0 + k;
+            if (lane == 0) base = atomicAdd(&blist[0], __popc(bm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (has) {
+                const int ic[3] = {t % g.n[0], (t / g.n[0]) % g.n[1], t / (g.n[0] * g.n[1])};
+                blist[1 + base + __popc(bm & lanemask_lt())] =
+                    (ic[0] + g.off[0]) + g.ext[0] * ((ic[1] + g.off[1]) + g.ext[1] * (ic[2] + g.off[2]));
+            }
         }
     }
     // ghost messages, one direction at a time over the directions any lane needs
@@ -260,7 +211,8 @@ __global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restri
 // ---- row a9: one-sided local-ghost forces ------------------------------------------------
 // Local particle i in a boundary cell sums f_ij over the ghosts j of its halo neighbour
 // cells; the peer rank computes the exact negation for its own copy (global ids key the
-// RNG, C-19).  Runs after the interior pass on the same stream: plain read-modify-write.
+// RNG, C-19).  Runs after the interior pass on the same stream.
+//
 // Halo neighbour cell d (0..26 = dir_index) of interior cell ci: extended-grid index and the
 // periodic shift of its ghosts; -1 if the cell is not in the halo ring.
 __device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, float sh[3])
@@ -289,109 +241,125 @@ __device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, 
     return halo ? e[0] + g.ext[0] * (e[1] + g.ext[1] * e[2]) : -1;
 }
 
-// One local-ghost pair (one-sided: the force on local i only).
-template <int KMODE>
-__device__ __forceinline__ void halo_pair(const float4 &pi, const float4 &vi, const float4 &pj, const float4 &vj,
-                                          const float sh[3], const PairP &pp, uint32_t ks, float &Fx, float &Fy,
-                                          float &Fz)
-{
-    const float rx = pi.x - (pj.x + sh[0]), ry = pi.y - (pj.y + sh[1]), rz = pi.z - (pj.z + sh[2]);
-    const float r2 = rx * rx + ry * ry + rz * rz;
-    const float dv = rx * (vi.x - vj.x) + ry * (vi.y - vj.y) + rz * (vi.z - vj.z);
-    const float s = pair_scalar<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(pi.w), (uint32_t)__float_as_int(pj.w), ks,
-                                       vi.w, vj.w);
-    Fx += s * rx;
-    Fy += s * ry;
-    Fz += s * rz;
-}
+// ---- row a9, warp per boundary cell ------------------------------------------------------
+// One warp per boundary cell of the list above: its local particles (<= 32 per pass, held
+// one per lane) against the ghosts of its halo neighbour cells.  The (particle, ghost)
+// combinations of one halo cell are spread over the lanes 32 at a time (i broadcast by
+// shuffle, the ghost gathered from L2), in-cutoff combinations are compacted into a per-warp
+// queue and evaluated 32 at a time -- every lane busy in both phases.  One-sided (C-19): the
+// i-side sums go to fixed-point shared accumulators, then once to frc.
+constexpr int kHcWarps = 4;
 
-constexpr int kHaloThreads = 128;
-constexpr int kHaloCap = 24; // hits kept per boundary particle before evaluating in place (mean ~6-12)
-
-// Halo forces of local particle i: all ghosts j of its halo neighbour cells (one-sided).
-// Two passes: the distance sweep collects the hits (ghost index | neighbour code << 27) in
-// the thread's shared-memory list, then the pair bodies run back to back -- the heavy pair
-// body is not executed for every candidate a neighbour lane hits.
 template <int KMODE>
-__device__ __forceinline__ void halo_particle(int i, const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                                              float4 *__restrict__ frc, const float4 *__restrict__ gpos,
-                                              const float4 *__restrict__ gvel, const int *__restrict__ gstart,
-                                              const Geom &g, const PairP &pp, uint32_t ks, unsigned *hl)
+__global__ void __launch_bounds__(32 * kHcWarps)
+    k_force_halo_cells(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
+                       const int *__restrict__ bcells, const int *__restrict__ start,
+                       const float4 *__restrict__ gpos, const float4 *__restrict__ gvel,
+                       const int *__restrict__ gstart, Geom g, PairP pp, float scale, float inv_scale,
+                       uint32_t s_lo, uint32_t s_hi)
 {
-    const float4 pi = pos[i];
-    const int ci[3] = {cell_coord(pi.x, g.inv_h[0], g.n[0]), cell_coord(pi.y, g.inv_h[1], g.n[1]),
-                       cell_coord(pi.z, g.inv_h[2], g.n[2])};
-    const float4 vi = vel[i];
-    float Fx = 0.f, Fy = 0.f, Fz = 0.f;
-    int nh = 0;
-    for (int d = 0; d < 27; ++d) {
-        float sh[3];
-        const int c = halo_cell(g, ci, d, sh);
-        if (c < 0) continue;
-        for (int j = gstart[c]; j < gstart[c + 1]; ++j) {
-            const float4 pj = gpos[j];
-            const float rx = pi.x - (pj.x + sh[0]), ry = pi.y - (pj.y + sh[1]), rz = pi.z - (pj.z + sh[2]);
-            const float r2 = rx * rx + ry * ry + rz * rz;
-            if (r2 < pp.rc2 && r2 > 0.0f) {
-                if (nh < kHaloCap) {
-                    hl[nh * kHaloThreads] = (unsigned)j | ((unsigned)d << 27);
-                    ++nh;
-                } else {
-                    halo_pair<KMODE>(pi, vi, pj, gvel[j], sh, pp, ks, Fx, Fy, Fz);
-                }
+    __shared__ unsigned qbuf[kHcWarps][64];
+    __shared__ int acc[kHcWarps][3][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned *q = qbuf[warp];
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
+    const int nbc = bcells[0];
+    for (int w = blockIdx.x * kHcWarps + warp; w < nbc; w += gridDim.x * kHcWarps) {
+        const int gc = bcells[1 + w];
+        const int ci[3] = {gc % g.ext[0] - g.off[0], (gc / g.ext[0]) % g.ext[1] - g.off[1],
+                           gc / (g.ext[0] * g.ext[1]) - g.off[2]};
+        const int s0 = start[gc], ntot = start[gc + 1] - s0;
+        // halo neighbour d of this cell on lane d: ghost range and periodic shift
+        int ha = 0, hn = 0;
+        float hsh[3] = {0.0f, 0.0f, 0.0f};
+        if (lane < 27) {
+            const int c = halo_cell(g, ci, lane, hsh);
+            if (c >= 0) {
+                ha = gstart[c];
+                hn = gstart[c + 1] - ha;
             }
         }
+        const unsigned hmask = __ballot_sync(0xffffffffu, hn > 0);
+        for (int ib = 0; ib < ntot; ib += 32) {
+            const int ni = min(32, ntot - ib);
+            float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
+            if (lane < ni) {
+                pi = pos[s0 + ib + lane];
+                vi = vel[s0 + ib + lane];
+            }
+            acc[warp][0][lane] = acc[warp][1][lane] = acc[warp][2][lane] = 0;
+            __syncwarp();
+            int qn = 0;
+            // evaluate queue entries [0, cnt): lane k takes entry k
+            auto evaluate = [&](int cnt) {
+                const unsigned e = lane < cnt ? q[lane] : 0u;
+                const int j = (int)(e & 0x3FFFFFu), ii = (int)((e >> 22) & 31u), d = (int)(e >> 27);
+                const float ix = __shfl_sync(0xffffffffu, pi.x, ii), iy = __shfl_sync(0xffffffffu, pi.y, ii),
+                            iz = __shfl_sync(0xffffffffu, pi.z, ii), iw = __shfl_sync(0xffffffffu, pi.w, ii);
+                const float ux = __shfl_sync(0xffffffffu, vi.x, ii), uy = __shfl_sync(0xffffffffu, vi.y, ii),
+                            uz = __shfl_sync(0xffffffffu, vi.z, ii), uw = __shfl_sync(0xffffffffu, vi.w, ii);
+                const float shx = __shfl_sync(0xffffffffu, hsh[0], d), shy = __shfl_sync(0xffffffffu, hsh[1], d),
+                            shz = __shfl_sync(0xffffffffu, hsh[2], d);
+                if (lane < cnt) {
+                    const float4 pj = gpos[j], vj = gvel[j];
+                    const float rx = ix - (pj.x + shx), ry = iy - (pj.y + shy), rz = iz - (pj.z + shz);
+                    const float r2 = rx * rx + ry * ry + rz * rz;
+                    const float dv = rx * (ux - vj.x) + ry * (uy - vj.y) + rz * (uz - vj.z);
+                    const float sc = pair_scalar<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(iw),
+                                                        (uint32_t)__float_as_int(pj.w), ks, uw, vj.w);
+                    atomicAdd(&acc[warp][0][ii], __float_as_int(__fmaf_rn(sc * rx, scale, 12582912.0f)) - 0x4B400000);
+                    atomicAdd(&acc[warp][1][ii], __float_as_int(__fmaf_rn(sc * ry, scale, 12582912.0f)) - 0x4B400000);
+                    atomicAdd(&acc[warp][2][ii], __float_as_int(__fmaf_rn(sc * rz, scale, 12582912.0f)) - 0x4B400000);
+                }
+            };
+            unsigned m = hmask;
+            while (m) {
+                const int d = __ffs(m) - 1;
+                m &= m - 1;
+                const int a = __shfl_sync(0xffffffffu, ha, d), len = __shfl_sync(0xffffffffu, hn, d);
+                const float shx = __shfl_sync(0xffffffffu, hsh[0], d), shy = __shfl_sync(0xffffffffu, hsh[1], d),
+                            shz = __shfl_sync(0xffffffffu, hsh[2], d);
+                const int P = ni * len;
+                const float inv_len = 1.0f / (float)len;
+                for (int base = 0; base < P; base += 32) {
+                    const int k = base + lane;
+                    int ii = (int)(((float)k + 0.5f) * inv_len);
+                    ii = min(ii, 31);
+                    const int jj = k - ii * len;
+                    const float ix = __shfl_sync(0xffffffffu, pi.x, ii), iy = __shfl_sync(0xffffffffu, pi.y, ii),
+                                iz = __shfl_sync(0xffffffffu, pi.z, ii);
+                    bool hit = false;
+                    if (k < P) {
+                        const float4 pj = gpos[a + jj];
+                        const float rx = ix - (pj.x + shx), ry = iy - (pj.y + shy), rz = iz - (pj.z + shz);
+                        const float r2 = rx * rx + ry * ry + rz * rz;
+                        hit = r2 < pp.rc2 && r2 > 0.0f;
+                    }
+                    const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                    if (hit) q[qn + __popc(hm & lanemask_lt())] = (unsigned)(a + jj) | ((unsigned)ii << 22) | ((unsigned)d << 27);
+                    qn += __popc(hm);
+                    __syncwarp();
+                    if (qn >= 32) {
+                        evaluate(32);
+                        __syncwarp();
+                        if (lane < qn - 32) q[lane] = q[32 + lane];
+                        qn -= 32;
+                        __syncwarp();
+                    }
+                }
+            }
+            if (qn > 0) evaluate(qn);
+            __syncwarp();
+            if (lane < ni) {
+                float4 f = frc[s0 + ib + lane];
+                f.x += (float)acc[warp][0][lane] * inv_scale;
+                f.y += (float)acc[warp][1][lane] * inv_scale;
+                f.z += (float)acc[warp][2][lane] * inv_scale;
+                frc[s0 + ib + lane] = f;
+            }
+            __syncwarp();
+        }
     }
-    for (int k = 0; k < nh; ++k) {
-        const unsigned e = hl[k * kHaloThreads];
-        const int j = (int)(e & 0x07FFFFFFu);
-        float sh[3];
-        halo_cell(g, ci, (int)(e >> 27), sh);
-        halo_pair<KMODE>(pi, vi, gpos[j], gvel[j], sh, pp, ks, Fx, Fy, Fz);
-    }
-    float4 f = frc[i];
-    f.x += Fx;
-    f.y += Fy;
-    f.z += Fz;
-    frc[i] = f;
-}
-
-template <int KMODE>
-__global__ void __launch_bounds__(kHaloThreads) k_force_halo(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                                                    float4 *__restrict__ frc, const int *__restrict__ n_ptr,
-                                                    const float4 *__restrict__ gpos, const float4 *__restrict__ gvel,
-                                                    const int *__restrict__ gstart, Geom g, PairP pp,
-                                                    uint32_t s_lo, uint32_t s_hi)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= *n_ptr) return;
-    const float4 pi = pos[i];
-    const int ci[3] = {cell_coord(pi.x, g.inv_h[0], g.n[0]), cell_coord(pi.y, g.inv_h[1], g.n[1]),
-                       cell_coord(pi.z, g.inv_h[2], g.n[2])};
-    bool boundary = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) boundary |= g.split[k] && (ci[k] == 0 || ci[k] == g.n[k] - 1);
-    __shared__ unsigned hl[kHaloThreads * kHaloCap];
-    if (!boundary) return;
-    halo_particle<KMODE>(i, pos, vel, frc, gpos, gvel, gstart, g, pp, step_key(s_lo, s_hi, pp.seed_fold),
-                         hl + threadIdx.x);
-}
-
-// The same over the boundary list of k_ghost_pack_cells (blist[0] entries): every thread
-// busy, no pass over the interior particles.
-template <int KMODE>
-__global__ void __launch_bounds__(kHaloThreads) k_force_halo_list(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
-                                                         float4 *__restrict__ frc, const int *__restrict__ blist,
-                                                         const float4 *__restrict__ gpos,
-                                                         const float4 *__restrict__ gvel,
-                                                         const int *__restrict__ gstart, Geom g, PairP pp,
-                                                         uint32_t s_lo, uint32_t s_hi)
-{
-    __shared__ unsigned hl[kHaloThreads * kHaloCap];
-    const int nb = blist[0];
-    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += gridDim.x * blockDim.x)
-        halo_particle<KMODE>(blist[1 + t], pos, vel, frc, gpos, gvel, gstart, g, pp, ks, hl + threadIdx.x);
 }
 
 } // namespace dpd
