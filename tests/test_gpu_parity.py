@@ -244,6 +244,23 @@ def test_temperature_rho8():
     assert abs(T - cfg.kT) < 0.01 * cfg.kT, T
 
 
+def test_temperature_config2_full_size_1000_steps():
+    """North star: ensemble temperature within 1 % of kT over 1000 steps, at BASELINE config 2
+    itself (64^3, rho = 8, 2.1 M particles, Table-2 parameters), full-step velocities (C-14)."""
+    cfg = workloads.CONFIGS["eq64"]
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg)
+    d.set_particles(pos0, vel0)
+    d.step(200)
+    Ts = []
+    for _ in range(50):
+        d.step(20)
+        _, v = d.get_particles()
+        Ts.append(oracle.temperature(v))
+    T = float(np.mean(Ts))
+    assert abs(T - cfg.kT) < 0.01 * cfg.kT, T
+
+
 @pytest.mark.parametrize("a", [50.0, 10.0])
 def test_groot_warren_pressure_rho8(a):
     """Structure of the GPU-sampled ensemble: p = rho T + W / (3V) with the conservative virial
