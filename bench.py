@@ -52,12 +52,14 @@ def _factor3(n):
     return best[1]
 
 
-# Algorithmic work model.  Per unordered interacting pair the pair body needs
-# ~77 lane-instructions at minimum (Philox4x32-10 words: 9 rounds x (2 IMAD.WIDE + 2 LOP3)
-# + final round 2 + min/max 2 = 40; Box-Muller 9; geometry, weights, dissipative dot product,
-# magnitude and the two force updates 28); every candidate pair of the half stencil needs a
-# distance test of 7 (3 FADD, 3 FMUL/FFMA, 1 FSETP).
-INSTR_PER_PAIR = 77.0
+# Algorithmic work model, in scalar lane-instructions.  Per unordered
+# interacting pair (C-7 Philox2x32-10, k = 1/2): Philox words 10 x (IMAD.WIDE + LOP3) + id
+# min/max = 22; Box-Muller 2 I2F + FFMA + LG2 + SQRT + 2 FMUL + COS + FMUL = 9; geometry
+# dx (3) + r^2 (3) + RSQ + r + w + SQRT(w) = 10; dissipative dot product 6; magnitude and
+# scalar 6; fixed-point quantise and Newton-3 accumulation 3 FFMA + 6 IADD + 3 ATOMS = 12;
+# operand loads (entry, j position x3, j velocity+id) 5 -> 70.  Per candidate pair of the
+# half stencil a distance test of 7 (3 FADD, 3 FMUL/FFMA, 1 FSETP).
+INSTR_PER_PAIR = 70.0
 INSTR_PER_CANDIDATE = 7.0
 # bytes per particle and launch, SURVEY §8d byte model
 KERNEL_BYTES = {"bin": 56.0, "scatter": 88.0, "force": 48.0, "pack": 40.0, "gather": 60.0}
