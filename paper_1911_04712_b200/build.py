@@ -50,6 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd += ["-DDPD_HAVE_NCCL=1", "-I", inc]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("DPD_NVCC_FLAGS", "").split()  # tools/ab.sh variants (-D knobs)
     tmp = LIB + f".tmp{os.getpid()}"
     cmd += ["-o", tmp, os.path.join(CSRC, "dpd_capi.cu")]
     if lib:

@@ -2055,6 +2055,13 @@ int dpd_dump_open(dpd_ctx *c, const char *path_prefix, int queue_depth)
     CUDA_TRY(c, cudaEventCreateWithFlags(&d->staged_free, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventRecord(d->staged_free, c->stream));
     if (!c->copy_stream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    if (c->n_cap > 0) {
+        // staging block and pinned slots for the current capacity now, not inside the first
+        // dumping step (pinned allocations take tens of ms); dump_snapshot re-sizes on growth
+        d->cap = c->n_cap;
+        CUDA_TRY(c, cudaMalloc(&d->dev, dump_bytes(d->cap)));
+        for (auto &sl : d->slots) CUDA_TRY(c, cudaMallocHost(&sl.host, dump_bytes(d->cap)));
+    }
     d->q = new dpd::IoQueue(queue_depth);
     c->dump = d;
     return DPD_OK;

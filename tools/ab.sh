@@ -9,7 +9,7 @@ for v in "$@"; do
   touch paper_1911_04712_b200/libdpd.so
   for rep in 1 2; do
     timeout 300 python bench.py --steps 200 --warmup 20 --no-cpu-baseline --no-e2e $BENCH_ARGS > gpurun_out/ab_${tag}_$(basename $v .so)_$rep.json 2>/dev/null
-    echo "$(basename $v) rep$rep: $(python tools/bench_brief.py gpurun_out/ab_${tag}_$(basename $v .so)_$rep.json | tail -1)"
+    echo "$(basename $v) rep$rep: $(python tools/bench_brief.py gpurun_out/ab_${tag}_$(basename $v .so)_$rep.json | tr "\n" " ")"
   done
 done
 cp /tmp/libdpd_orig.so paper_1911_04712_b200/libdpd.so
