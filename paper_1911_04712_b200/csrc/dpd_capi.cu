@@ -12,10 +12,10 @@
 //          k_bin_recv     received migrants -> histogram
 //   a3     k_scan         exclusive scan of the counts
 //   a4     k_scatter (+ k_scatter_recv)  cell-sorted copy
-//   a7     k_ghost_pack   boundary-layer particles -> ghost messages
+//   a7     k_ghost_pack_cells   boundary-layer particles -> ghost messages
 //   a8     exchange(ghost) on the comm stream, overlapped with
 //   a5     k_force_tile   local-local half-stencil pairs
-//   a9     k_ghost_bin/scan/scatter + k_force_halo   one-sided local-ghost pairs
+//   a9     k_ghost_bin/scan/scatter + k_force_halo_cells   one-sided local-ghost pairs
 #include <cuda_runtime.h>
 
 #include <algorithm>
