@@ -136,3 +136,38 @@ def test_group_temperature_and_momentum():
         assert np.abs(np.array(Ps)).max() < 1e-2 * np.sqrt(pos0.shape[0])
     finally:
         destroy(capi, ctxs)
+
+
+def test_group_full_size_sampled_parity():
+    """2x2x2 group over BASELINE config 4's 128^3 box at rho = 8 (16.8 M particles, 64^3 per
+    subdomain as in bench's multi-GPU weak run): after the prime and 3 steps with migration,
+    sampled all-j force sums (local + halo pairs) against the oracle's plain definition (C-1),
+    every id present exactly once, sum F = 0."""
+    cfg = workloads.CONFIGS["weak128"]
+    p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
+                         seed=cfg.seed)
+    pos0, vel0 = workloads.make_config(cfg)
+    n = pos0.shape[0]
+    capi, ctxs = make_group(cfg, (2, 2, 2))
+    try:
+        ids0 = np.arange(n, dtype=np.int32)
+        for c in ctxs:
+            capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
+        capi.dpd_group_step(ctxs, 0)
+        capi.dpd_group_step(ctxs, 3)
+        steps = {capi.dpd_get_step(c) for c in ctxs}
+        assert len(steps) == 1
+        pos, u, f, ids = gather_state(capi, ctxs)
+        assert pos.shape[0] == n and np.array_equal(np.sort(ids), ids0)
+        # boundary particles sit in the halo of up to 7 other subdomains: sample those too
+        rng = np.random.default_rng(7)
+        near = np.where(np.any(np.abs(np.mod(pos, 64.0) - 32.0) > 31.0, axis=1))[0]
+        sel = np.concatenate([rng.choice(n, 16, replace=False), rng.choice(near, 16, replace=False)])
+        F_ref, allow = oracle.forces_subset(p, pos, u, steps.pop(), sel, ids=ids.astype(np.uint32),
+                                            eps=boundary_eps(cfg.box))
+        scale = np.abs(f).max()
+        err = np.abs(f[sel].astype(np.float64) - F_ref).max(axis=1)
+        assert np.all(err <= FORCE_TOL * scale + allow), (err.max(), scale)
+        assert np.abs(f.astype(np.float64).sum(0)).max() < 1e-5 * np.abs(f).sum()
+    finally:
+        destroy(capi, ctxs)
