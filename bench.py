@@ -7,7 +7,10 @@ of the step (SURVEY §8d byte model) and the dominant kernel's roofline.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config eq64] [--impl reference]
 
 N = 1 runs the BASELINE config 2 (64^3, rho = 8, 2,097,152 particles, P:483, P:489 params).
-N > 1 (under torchrun): weak scaling, one 64^3 subdomain per GPU on a 3D rank grid, NCCL.
+N > 1 (under torchrun): BASELINE config 4, weak scaling, one 128^3 subdomain per GPU
+(16,777,216 particles, same parameters) on a 3D rank grid, NCCL.  One GPU runs both sizes at
+the same per-particle rate (profiles/r01_bench_weak128.json), so the driver's efficiency
+from the per-N values measures the decomposition cost.
 Prints ONE JSON line on rank 0.  See DESIGN.md §8 for every field.
 """
 from __future__ import annotations
@@ -230,7 +233,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="eq64")
+    ap.add_argument("--config", default=None, help="workloads.CONFIGS name (default: eq64 at N = 1, weak128 at N > 1)")
     ap.add_argument("--impl", default="dpd", choices=["dpd", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -238,6 +241,8 @@ def main():
     ap.add_argument("--option", action="append", default=[], help="engine option name=value (dpd_set_option)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config is None:
+        args.config = "eq64" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "weak128"
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)

@@ -638,6 +638,17 @@ int exchange_nccl(dpd_ctx *c, MsgArea &m, cudaStream_t st)
 
 int exchange_group(dpd_ctx **g, int n, bool ghosts)
 {
+    // one k_group_copy launch per kCopyJobs messages (all members share one stream)
+    CopyJobs jobs;
+    int nj = 0;
+    auto flush = [&]() -> int {
+        if (nj == 0) return DPD_OK;
+        dpd_ctx *c = g[0];
+        TRY(launch(c, ghosts ? KID_GHOST_PACK : KID_MIGRATE,
+                   [&] { k_group_copy<<<dim3(16, nj), 256, 0, c->stream>>>(jobs); }));
+        nj = 0;
+        return DPD_OK;
+    };
     for (int r = 0; r < n; ++r) {
         dpd_ctx *c = g[r];
         MsgArea &m = ghosts ? c->gh : c->mig;
@@ -645,11 +656,14 @@ int exchange_group(dpd_ctx **g, int n, bool ghosts)
             if (m.bytes[d] == 0) continue;
             dpd_ctx *p = g[c->peer_to[d]];
             MsgArea &pm = ghosts ? p->gh : p->mig;
-            CUDA_TRY(c, cudaMemcpyAsync(pm.recv.p + pm.mr.off[d], m.send.p + m.ms.off[d], m.bytes[d],
-                                        cudaMemcpyDeviceToDevice, c->stream));
+            if (pm.mr.cap[d] != m.ms.cap[d]) return fail(c, DPD_ERR_CONFIG, "group message capacities differ");
+            jobs.j[nj].src = reinterpret_cast<const int4 *>(m.send.p + m.ms.off[d]);
+            jobs.j[nj].dst = reinterpret_cast<int4 *>(pm.recv.p + pm.mr.off[d]);
+            jobs.j[nj].cap = m.ms.cap[d];
+            if (++nj == kCopyJobs) TRY(flush());
         }
     }
-    return DPD_OK;
+    return flush();
 }
 
 // ---- message buffers ------------------------------------------------------------------------

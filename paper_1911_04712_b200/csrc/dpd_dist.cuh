@@ -18,6 +18,28 @@ __global__ void k_zero_headers(Msgs m)
     if (d < 27 && m.cap[d] > 0) *msg_count(m, d) = 0;
 }
 
+// In-process group transport: every (sender, direction) message of one exchange in one
+// launch (blockIdx.y = job).  Copies the int4 count header and the min(count, cap) particles
+// actually packed (two int4 each), not the capacity-padded slot; an overflowing count is
+// copied as is so the receiver raises ERR_CAPACITY (msg_received).
+constexpr int kCopyJobs = 512;
+struct CopyJob {
+    const int4 *src;
+    int4 *dst;
+    int cap;
+};
+struct CopyJobs {
+    CopyJob j[kCopyJobs];
+};
+
+__global__ void __launch_bounds__(256) k_group_copy(const __grid_constant__ CopyJobs jobs)
+{
+    const CopyJob &J = jobs.j[blockIdx.y];
+    const int cnt = min(max(J.src[0].x, 0), J.cap);
+    const int total = 1 + 2 * cnt;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) J.dst[k] = J.src[k];
+}
+
 __device__ __forceinline__ int msg_received(const Msgs &m, int d, int *err)
 {
     const int c = *msg_count(m, d);
@@ -243,10 +265,10 @@ __device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, 
 
 // ---- row a9, warp per boundary cell ------------------------------------------------------
 // One warp per boundary cell of the list above: its local particles (<= 32 per pass, held
-// one per lane) against the ghosts of its halo neighbour cells.  The (particle, ghost)
-// combinations of one halo cell are spread over the lanes 32 at a time (i broadcast by
-// shuffle, the ghost gathered from L2), in-cutoff combinations are compacted into a per-warp
-// queue and evaluated 32 at a time -- every lane busy in both phases.  One-sided (C-19): the
+// one per lane) against the ghosts of its halo neighbour cells, concatenated into one list
+// and taken 32 at a time (one ghost per lane, i broadcast by shuffle); in-cutoff combinations
+// are compacted into a per-warp queue and evaluated 32 at a time -- every lane busy in both
+// phases.  One-sided (C-19): the
 // i-side sums go to fixed-point shared accumulators, then once to frc.
 constexpr int kHcWarps = 4;
 
@@ -279,7 +301,15 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                 hn = gstart[c + 1] - ha;
             }
         }
-        const unsigned hmask = __ballot_sync(0xffffffffu, hn > 0);
+        // exclusive prefix of the halo cells' ghost counts over lanes 0..26
+        int hex = hn;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, hex, o);
+            if (lane >= o) hex += y;
+        }
+        const int G = __shfl_sync(0xffffffffu, hex, 31);
+        hex -= hn;
         for (int ib = 0; ib < ntot; ib += 32) {
             const int ni = min(32, ntot - ib);
             float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = pi;
@@ -312,31 +342,40 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                     atomicAdd(&acc[warp][2][ii], __float_as_int(__fmaf_rn(sc * rz, scale, 12582912.0f)) - 0x4B400000);
                 }
             };
-            unsigned m = hmask;
-            while (m) {
-                const int d = __ffs(m) - 1;
-                m &= m - 1;
-                const int a = __shfl_sync(0xffffffffu, ha, d), len = __shfl_sync(0xffffffffu, hn, d);
+            // the ghosts of all halo neighbour cells as one list, 32 per chunk with one ghost
+            // per lane (position shifted to the local frame once), tested against the cell's
+            // local particles one at a time (i broadcast by shuffle): the chunk's candidates
+            // cost a few instructions per lane-pair, no per-candidate index math or gather
+            for (int cb = 0; cb < G; cb += 32) {
+                const int gi = cb + lane;
+                int d = 0; // largest halo lane with prefix <= gi (the prefix is non-decreasing)
+#pragma unroll
+                for (int stp = 16; stp > 0; stp >>= 1) {
+                    const int t = d + stp;
+                    const int off_t = __shfl_sync(0xffffffffu, hex, t & 31);
+                    if (t < 27 && off_t <= gi) d = t;
+                }
+                const int a = __shfl_sync(0xffffffffu, ha, d), off = __shfl_sync(0xffffffffu, hex, d);
                 const float shx = __shfl_sync(0xffffffffu, hsh[0], d), shy = __shfl_sync(0xffffffffu, hsh[1], d),
                             shz = __shfl_sync(0xffffffffu, hsh[2], d);
-                const int P = ni * len;
-                const float inv_len = 1.0f / (float)len;
-                for (int base = 0; base < P; base += 32) {
-                    const int k = base + lane;
-                    int ii = (int)(((float)k + 0.5f) * inv_len);
-                    ii = min(ii, 31);
-                    const int jj = k - ii * len;
-                    const float ix = __shfl_sync(0xffffffffu, pi.x, ii), iy = __shfl_sync(0xffffffffu, pi.y, ii),
-                                iz = __shfl_sync(0xffffffffu, pi.z, ii);
-                    bool hit = false;
-                    if (k < P) {
-                        const float4 pj = gpos[a + jj];
-                        const float rx = ix - (pj.x + shx), ry = iy - (pj.y + shy), rz = iz - (pj.z + shz);
-                        const float r2 = rx * rx + ry * ry + rz * rz;
-                        hit = r2 < pp.rc2 && r2 > 0.0f;
-                    }
+                const bool gv = gi < G;
+                const unsigned jidx = gv ? (unsigned)(a + gi - off) : 0u;
+                float px = 3.0e30f, py = 0.0f, pz = 0.0f; // invalid lane: never within r_c
+                if (gv) {
+                    const float4 pj = gpos[jidx];
+                    px = pj.x + shx;
+                    py = pj.y + shy;
+                    pz = pj.z + shz;
+                }
+                const unsigned tag = jidx | ((unsigned)d << 27);
+                for (int ii = 0; ii < ni; ++ii) {
+                    const float rx = __shfl_sync(0xffffffffu, pi.x, ii) - px;
+                    const float ry = __shfl_sync(0xffffffffu, pi.y, ii) - py;
+                    const float rz = __shfl_sync(0xffffffffu, pi.z, ii) - pz;
+                    const float r2 = rx * rx + ry * ry + rz * rz;
+                    const bool hit = r2 < pp.rc2 && r2 > 0.0f;
                     const unsigned hm = __ballot_sync(0xffffffffu, hit);
-                    if (hit) q[qn + __popc(hm & lanemask_lt())] = (unsigned)(a + jj) | ((unsigned)ii << 22) | ((unsigned)d << 27);
+                    if (hit) q[qn + __popc(hm & lanemask_lt())] = tag | ((unsigned)ii << 22);
                     qn += __popc(hm);
                     __syncwarp();
                     if (qn >= 32) {
