@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                        const int *__restrict__ gstart, Geom g, PairP pp, float scale, float inv_scale,
                        uint32_t s_lo, uint32_t s_hi)
 {
-    __shared__ unsigned qbuf[kHcWarps][64];
+    __shared__ unsigned qbuf[kHcWarps][96]; // < 32 pending + 2 x 32 new
     __shared__ int acc[kHcWarps][3][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned *q = qbuf[warp];
@@ -368,20 +368,27 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                     pz = pj.z + shz;
                 }
                 const unsigned tag = jidx | ((unsigned)d << 27);
-                for (int ii = 0; ii < ni; ++ii) {
-                    const float rx = __shfl_sync(0xffffffffu, pi.x, ii) - px;
-                    const float ry = __shfl_sync(0xffffffffu, pi.y, ii) - py;
-                    const float rz = __shfl_sync(0xffffffffu, pi.z, ii) - pz;
-                    const float r2 = rx * rx + ry * ry + rz * rz;
-                    const bool hit = r2 < pp.rc2 && r2 > 0.0f;
-                    const unsigned hm = __ballot_sync(0xffffffffu, hit);
-                    if (hit) q[qn + __popc(hm & lanemask_lt())] = tag | ((unsigned)ii << 22);
-                    qn += __popc(hm);
+                for (int ii = 0; ii < ni; ii += 2) { // two local particles per round
+                    const int i1 = min(ii + 1, 31);
+                    const float ax = __shfl_sync(0xffffffffu, pi.x, ii) - px;
+                    const float ay = __shfl_sync(0xffffffffu, pi.y, ii) - py;
+                    const float az = __shfl_sync(0xffffffffu, pi.z, ii) - pz;
+                    const float bx = __shfl_sync(0xffffffffu, pi.x, i1) - px;
+                    const float by = __shfl_sync(0xffffffffu, pi.y, i1) - py;
+                    const float bz = __shfl_sync(0xffffffffu, pi.z, i1) - pz;
+                    const float ra = ax * ax + ay * ay + az * az, rb = bx * bx + by * by + bz * bz;
+                    const bool ha = ra < pp.rc2 && ra > 0.0f;
+                    const bool hb = ii + 1 < ni && rb < pp.rc2 && rb > 0.0f;
+                    const unsigned ma = __ballot_sync(0xffffffffu, ha), mb = __ballot_sync(0xffffffffu, hb);
+                    const unsigned lt = lanemask_lt();
+                    if (ha) q[qn + __popc(ma & lt)] = tag | ((unsigned)ii << 22);
+                    if (hb) q[qn + __popc(ma) + __popc(mb & lt)] = tag | ((unsigned)(ii + 1) << 22);
+                    qn += __popc(ma) + __popc(mb);
                     __syncwarp();
-                    if (qn >= 32) {
+                    while (qn >= 32) {
                         evaluate(32);
                         __syncwarp();
-                        if (lane < qn - 32) q[lane] = q[32 + lane];
+                        for (int k = lane; k < qn - 32; k += 32) q[k] = q[k + 32];
                         qn -= 32;
                         __syncwarp();
                     }
