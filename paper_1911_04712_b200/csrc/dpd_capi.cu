@@ -434,9 +434,9 @@ int phase_ghost_pack(dpd_ctx *c)
     CUDA_TRY(c, c->blist.reserve((size_t)g.ncell + 1));
     CUDA_TRY(c, cudaMemsetAsync(c->blist.p, 0, sizeof(int), c->stream));
     TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(gs); }));
-    const int ncell_in = g.n[0] * g.n[1] * g.n[2];
+    const dim3 grid((g.n[0] + kGpThreads - 1) / kGpThreads, g.n[1], g.n[2]);
     return launch(c, KID_GHOST_PACK, [&] {
-        k_ghost_pack_cells<<<nblk(ncell_in, 256), 256, 0, c->stream>>>(c->pos[c->cur].p, c->vel[c->cur].p,
+        k_ghost_pack_cells<<<grid, kGpThreads, 0, c->stream>>>(c->pos[c->cur].p, c->vel[c->cur].p,
                                                                         c->start[c->scur].p, g, gs, c->blist.p,
                                                                         c->err.p);
     });

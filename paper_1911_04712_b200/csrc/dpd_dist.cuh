@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) k_ghost_scatter(Msgs rec, Geom g, int max
     gvel[dst] = msg_data(rec, d)[2 * k + 1];
 }
 
-// ---- row a7: ghost identify + pack, one thread per interior cell ---------------------------
+// ---- row a7: ghost identify + pack, one thread per interior cell (3D grid) -----------------
 // Only the cells of the boundary layers of split dimensions do work (~5 % at 128^3 per
 // rank).  A boundary cell's particles (contiguous in the sorted arrays) are written to every
 // direction its position calls for (face / edge / corner: a corner cell's particles go to 7
@@ -146,39 +146,37 @@ __global__ void __launch_bounds__(256) k_ghost_scatter(Msgs rec, Geom g, int max
 // reservation per direction; the cell itself is appended to the boundary-cell list
 // blist[1..blist[0]] that drives the halo force (row a9).  The order inside a message is
 // irrelevant: the receiver bins the ghosts into its halo ring.
-__global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restrict__ pos,
-                                                          const float4 *__restrict__ vel,
-                                                          const int *__restrict__ start, Geom g, Msgs gs,
-                                                          int *__restrict__ blist, int *err)
+constexpr int kGpThreads = 128; // x-extent of a block; grid (ceil(n_x / 128), n_y, n_z)
+
+__global__ void __launch_bounds__(kGpThreads) k_ghost_pack_cells(const float4 *__restrict__ pos,
+                                                                 const float4 *__restrict__ vel,
+                                                                 const int *__restrict__ start, Geom g, Msgs gs,
+                                                                 int *__restrict__ blist, int *err)
 {
-    const int ncell = g.n[0] * g.n[1] * g.n[2];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    const int ic[3] = {(int)(blockIdx.x * kGpThreads + threadIdx.x), (int)blockIdx.y, (int)blockIdx.z};
     unsigned dmask = 0;
-    int s0 = 0, cnt = 0;
+    int s0 = 0, cnt = 0, gc = 0;
     bool border = false;
-    if (t < ncell) {
-        const int ic[3] = {t % g.n[0], (t / g.n[0]) % g.n[1], t / (g.n[0] * g.n[1])};
-        int lo[3], hi[3];
+    if (ic[0] < g.n[0]) {
+        int sd[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            lo[k] = g.split[k] && ic[k] == 0;
-            hi[k] = g.split[k] && ic[k] == g.n[k] - 1;
-            border = border || lo[k] || hi[k];
+            sd[k] = !g.split[k] ? 0 : (ic[k] == 0 ? -1 : (ic[k] == g.n[k] - 1 ? 1 : 0));
+            border = border || sd[k] != 0;
         }
         if (border) {
-            const int gc = (ic[0] + g.off[0]) + g.ext[0] * ((ic[1] + g.off[1]) + g.ext[1] * (ic[2] + g.off[2]));
+            gc = (ic[0] + g.off[0]) + g.ext[0] * ((ic[1] + g.off[1]) + g.ext[1] * (ic[2] + g.off[2]));
             s0 = start[gc];
             cnt = start[gc + 1] - s0;
-            for (int dz = -1; dz <= 1; ++dz)
-                for (int dy = -1; dy <= 1; ++dy)
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        const int d = dir_index(dx, dy, dz);
-                        if (d == 13 || gs.cap[d] == 0) continue;
-                        if ((dx == 0 || (dx < 0 ? lo[0] : hi[0])) && (dy == 0 || (dy < 0 ? lo[1] : hi[1])) &&
-                            (dz == 0 || (dz < 0 ? lo[2] : hi[2])))
-                            dmask |= 1u << d;
-                    }
+            // directions: every non-empty combination of this cell's face offsets (a face
+            // cell 1, an edge cell 3, a corner cell 7); all of them are used (split) directions
+#pragma unroll
+            for (int m = 1; m < 8; ++m) {
+                const int dx = (m & 1) ? sd[0] : 0, dy = (m & 2) ? sd[1] : 0, dz = (m & 4) ? sd[2] : 0;
+                const bool ok = ((m & 1) == 0 || dx) && ((m & 2) == 0 || dy) && ((m & 4) == 0 || dz);
+                if (ok) dmask |= 1u << dir_index(dx, dy, dz);
+            }
         }
     }
     // boundary-cell list (extended-grid index of every non-empty boundary cell)
@@ -189,11 +187,7 @@ __global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restri
             int base = 0;
             if (lane == 0) base = atomicAdd(&blist[0], __popc(bm));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (has) {
-                const int ic[3] = {t % g.n[0], (t / g.n[0]) % g.n[1], t / (g.n[0] * g.n[1])};
-                blist[1 + base + __popc(bm & lanemask_lt())] =
-                    (ic[0] + g.off[0]) + g.ext[0] * ((ic[1] + g.off[1]) + g.ext[1] * (ic[2] + g.off[2]));
-            }
+            if (has) blist[1 + base + __popc(bm & lanemask_lt())] = gc;
         }
     }
     // ghost messages, one direction at a time over the directions any lane needs
@@ -216,16 +210,16 @@ __global__ void __launch_bounds__(256) k_ghost_pack_cells(const float4 *__restri
             const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
             const float shx = dx * g.L[0], shy = dy * g.L[1], shz = dz * g.L[2];
             float4 *q = msg_data(gs, d);
-            for (int k = 0; k < v; ++k) {
-                const int slot = base + incl - v + k;
-                const float4 p = pos[s0 + k];
-                if (slot < gs.cap[d]) {
-                    q[2 * slot] = make_float4(p.x - shx, p.y - shy, p.z - shz, p.w);
-                    q[2 * slot + 1] = vel[s0 + k];
-                } else {
-                    raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
-                }
+            const int slot0 = base + incl - v;
+            const int vfit = max(0, min(v, gs.cap[d] - slot0)); // overflow: counted, not written
+            // no branch in the copy loop: the loads of several particles are in flight
+#pragma unroll 4
+            for (int k = 0; k < vfit; ++k) {
+                const float4 p = pos[s0 + k], u = vel[s0 + k];
+                q[2 * (slot0 + k)] = make_float4(p.x - shx, p.y - shy, p.z - shz, p.w);
+                q[2 * (slot0 + k) + 1] = u;
             }
+            if (vfit < v) raise_err(err, ERR_CAPACITY, __float_as_int(pos[s0 + vfit].w));
         }
     }
 }
