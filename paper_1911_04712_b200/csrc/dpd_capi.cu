@@ -1551,7 +1551,9 @@ int dpd_set_particles_typed(dpd_ctx *c, int64_t n, const float *pos, const float
     c->step = step0;
     c->cur = 0;
     c->scur = 0;
-    const size_t words = (size_t)std::max<int64_t>(n, 1) * 8;
+    // 8 words per particle for this upload; 10 covers every getter (gather 9, forces 10), so a
+    // first get does not re-allocate (cudaFree + cudaMalloc synchronise the device)
+    const size_t words = (size_t)std::max<int64_t>(n, 1) * 10;
     CUDA_TRY(c, c->stage.reserve(words));
     float *d_pos = c->stage.p, *d_vel = c->stage.p + 3 * (size_t)n;
     int32_t *d_ids = ids ? reinterpret_cast<int32_t *>(c->stage.p + 6 * (size_t)n) : nullptr;
