@@ -10,7 +10,8 @@ N = 1 runs the BASELINE config 2 (64^3, rho = 8, 2,097,152 particles, P:483, P:4
 N > 1 (under torchrun): BASELINE config 4, weak scaling, one 128^3 subdomain per GPU
 (16,777,216 particles, same parameters) on a 3D rank grid, NCCL.  One GPU runs both sizes at
 the same per-particle rate (profiles/r01_bench_weak128.json), so the driver's efficiency
-from the per-N values measures the decomposition cost.
+from the per-N values measures the decomposition cost.  `--config strong256 --scaling strong`
+runs BASELINE config 5 instead: the fixed 256^3 box split over the N GPUs.
 Prints ONE JSON line on rank 0.  See DESIGN.md §8 for every field.
 """
 from __future__ import annotations
@@ -219,10 +220,13 @@ def run_reference(args, cfg):
 
 def config_block(cfg, args, world):
     g = rank_grid(world)
-    return {"workload": f"{cfg.name}: periodic DPD box {cfg.box[0]:g}x{cfg.box[1]:g}x{cfg.box[2]:g} per GPU, "
+    strong = getattr(args, "scaling", "weak") == "strong"
+    where = "in total, split over the GPUs" if strong else "per GPU"
+    return {"workload": f"{cfg.name}: periodic DPD box {cfg.box[0]:g}x{cfg.box[1]:g}x{cfg.box[2]:g} {where}, "
                         f"rho={cfg.rho:g}, a={cfg.a:g}, gamma={cfg.gamma:g}, kT={cfg.kT:g}, k={cfg.power:g}, "
                         f"dt={cfg.dt:g}, rc={cfg.rc:g}",
-            "particles_per_gpu": cfg.n, "particles_total": cfg.n * world,
+            "particles_per_gpu": cfg.n // world if strong else cfg.n,
+            "particles_total": cfg.n if strong else cfg.n * world,
             "rank_grid": list(g), "parallelism": f"domain-decomposition {g[0]}x{g[1]}x{g[2]}",
             "l2": "inputs larger than L2: double-buffered state ~%.0f MB > 126 MB L2; no flush" %
                   (cfg.n * 96 / 1e6)}
@@ -235,6 +239,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default=None, help="workloads.CONFIGS name (default: eq64 at N = 1, weak128 at N > 1)")
     ap.add_argument("--impl", default="dpd", choices=["dpd", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the config's box per GPU (default); strong: the config's box split over the GPUs "
+                         "(BASELINE config 5: --config strong256 --scaling strong)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-kernel", type=int, default=None, help="0 tiled, 1 reference, 2 cell-warp")
@@ -258,7 +265,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     grid = rank_grid(world)
-    gbox = tuple(cfg.box[k] * grid[k] for k in range(3))
+    strong = args.scaling == "strong"
+    gbox = tuple(cfg.box[k] if strong else cfg.box[k] * grid[k] for k in range(3))
+    sub = tuple(gbox[k] / grid[k] for k in range(3))  # this rank's subdomain
     stream = torch.cuda.Stream()
 
     # --- build the context and the workload -------------------------------------------------
@@ -287,8 +296,8 @@ def main():
         capi.dpd_set_body_force(ctx, cfg.body_f)
     # each rank generates only its own subdomain's particles with globally unique ids
     coord = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
-    pos, vel = workloads.make_particles(cfg.box, cfg.rho, cfg.kT, init_seed=1 + rank)
-    pos = (pos + np.array([coord[k] * cfg.box[k] for k in range(3)], np.float32)).astype(np.float32)
+    pos, vel = workloads.make_particles(sub, cfg.rho, cfg.kT, init_seed=1 + rank)
+    pos = (pos + np.array([coord[k] * sub[k] for k in range(3)], np.float32)).astype(np.float32)
     n_local = pos.shape[0]
     ids = (np.arange(n_local, dtype=np.int64) + rank * n_local).astype(np.int32)
     pos_h = torch.from_numpy(pos).pin_memory()
@@ -381,7 +390,7 @@ def main():
                 t["dram_bytes"] / max(1.0, KERNEL_BYTES.get(dom, 0.0) * n_local)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
            "vs_baseline": None, "dtype": "f32", "data": "synthetic: uniform positions, Maxwell-Boltzmann velocities",
            "config": config_block(cfg, args, world), "clocks": clocks.summary(), "gpu_launches": launches,
            "roofline": roof,
