@@ -298,6 +298,9 @@ def main():
     coord = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
     pos, vel = workloads.make_particles(sub, cfg.rho, cfg.kT, init_seed=1 + rank)
     pos = (pos + np.array([coord[k] * sub[k] for k in range(3)], np.float32)).astype(np.float32)
+    for k in range(3):  # the shift can round up onto the next subdomain's face: keep it local
+        hi = np.float32((coord[k] + 1) * sub[k])
+        pos[pos[:, k] >= hi, k] = np.nextafter(hi, np.float32(0.0))
     n_local = pos.shape[0]
     ids = (np.arange(n_local, dtype=np.int64) + rank * n_local).astype(np.int32)
     pos_h = torch.from_numpy(pos).pin_memory()
