@@ -260,20 +260,21 @@ cudaEvent_t get_event(dpd_ctx *c)
 
 // Launch helper: optional event pair around the launch, launch counting, error check.
 template <class F>
-int launch(dpd_ctx *c, int kid, F &&f)
+int launch(dpd_ctx *c, int kid, F &&f, cudaStream_t st = nullptr)
 {
+    if (!st) st = c->stream; // the stream f() launches on (timing events go there too)
     cudaEvent_t a = nullptr, b = nullptr;
     if (c->timing) {
         a = get_event(c);
         b = get_event(c);
-        cudaEventRecord(a, c->stream);
+        cudaEventRecord(a, st);
     }
     f();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         return fail(c, DPD_ERR_CUDA, "launch of %s failed: %s", kKernelNames[kid], cudaGetErrorString(e));
     if (c->timing) {
-        cudaEventRecord(b, c->stream);
+        cudaEventRecord(b, st);
         c->pending.push_back({a, b, kid});
     }
     c->launches += 1;
@@ -572,24 +573,37 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     });
 }
 
-// a9: received ghosts -> halo cells, then one-sided local-ghost forces.
-int phase_halo(dpd_ctx *c, int64_t step)
+// a9 (first half): received ghosts -> halo cells (bin, scan, scatter) on stream st.  Touches
+// only ghost buffers, so in the step graph it runs on the communication stream right after
+// the exchange, concurrently with the local forces.
+int phase_ghost_sort(dpd_ctx *c, cudaStream_t st)
 {
     const Geom g = c->geom;
     const Msgs gr = c->gh.mr;
     const dim3 grid(nblk(c->gh.maxcap, 256), 27);
-    TRY(launch(c, KID_GHOST_SORT, [&] {
-        k_ghost_bin<<<grid, 256, 0, c->stream>>>(gr, g, c->gh.maxcap, c->gcount.p, c->grank.p, c->err.p);
-    }));
+    TRY(launch(
+        c, KID_GHOST_SORT,
+        [&] { k_ghost_bin<<<grid, 256, 0, st>>>(gr, g, c->gh.maxcap, c->gcount.p, c->grank.p, c->err.p); }, st));
     const int ntile = (g.ncell + kScanTile - 1) / kScanTile;
-    TRY(launch(c, KID_GHOST_SORT, [&] {
-        k_scan<<<ntile, kScanThreads, 0, c->stream>>>(c->gcount.p, c->gstart.p, g.ncell, c->gscan_state.p,
-                                                      c->scan_epoch.p + 1);
-    }));
-    TRY(launch(c, KID_GHOST_SORT, [&] {
-        k_ghost_scatter<<<grid, 256, 0, c->stream>>>(gr, g, c->gh.maxcap, c->gstart.p, c->grank.p, c->gpos.p,
-                                                     c->gvel.p);
-    }));
+    TRY(launch(
+        c, KID_GHOST_SORT,
+        [&] {
+            k_scan<<<ntile, kScanThreads, 0, st>>>(c->gcount.p, c->gstart.p, g.ncell, c->gscan_state.p,
+                                                   c->scan_epoch.p + 1);
+        },
+        st));
+    return launch(
+        c, KID_GHOST_SORT,
+        [&] {
+            k_ghost_scatter<<<grid, 256, 0, st>>>(gr, g, c->gh.maxcap, c->gstart.p, c->grank.p, c->gpos.p, c->gvel.p);
+        },
+        st);
+}
+
+// a9 (second half): one-sided local-ghost forces (after the local forces, same stream).
+int phase_halo_force(dpd_ctx *c, int64_t step)
+{
+    const Geom g = c->geom;
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const PairP pp = c->pp;
     const int b = c->cur;
@@ -609,6 +623,13 @@ int phase_halo(dpd_ctx *c, int64_t step)
         }
 #undef DPD_HALO
     });
+}
+
+// a9 on the context's stream (prime, in-process group).
+int phase_halo(dpd_ctx *c, int64_t step)
+{
+    TRY(phase_ghost_sort(c, c->stream));
+    return phase_halo_force(c, step);
 }
 
 // ---- transports ---------------------------------------------------------------------------
@@ -863,8 +884,8 @@ int dump_copyout(dpd_ctx *c, cudaStream_t st)
 
 // ---- one step of one context as a task graph (NCCL or single) ----------------------------
 // Tasks (stream slot): kick_drift_bin (0) -> [migrate_exchange (0)] -> scan_scatter (0) ->
-// [ghost_pack (0) -> ghost_exchange (1, comm stream)] ; force_local (0) -> [halo_force (0),
-// after ghost_exchange] -> [snapshot (0) -> snapshot_d2h (2, copy stream)].  Kahn's order
+// [ghost_pack (0) -> ghost_exchange (1, comm stream) -> ghost_sort (1)] ; force_local (0) ->
+// [halo_force (0), after ghost_sort] -> [snapshot (0) -> snapshot_d2h (2, copy stream)].  Kahn's order
 // issues ghost_exchange before force_local, so the exchange overlaps the interior forces
 // (P:244-247); cross-stream edges become CUDA events.
 dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
@@ -893,6 +914,9 @@ dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
         g->edge(t_sort, t_gp);
         t_gx = g->add("ghost_exchange", 1, [c](cudaStream_t s) { return exchange_nccl(c, c->gh, s); });
         g->edge(t_gp, t_gx);
+        const int t_gs = g->add("ghost_sort", 1, [c](cudaStream_t s) { return phase_ghost_sort(c, s); });
+        g->edge(t_gx, t_gs);
+        t_gx = t_gs; // the halo forces wait for the sorted ghosts
     }
     const int t_force = g->add("force_local", 0, [c](cudaStream_t) {
         return force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false);
@@ -900,7 +924,7 @@ dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
     g->edge(t_sort, t_force);
     last = t_force;
     if (c->dist) {
-        const int t_h = g->add("halo_force", 0, [c](cudaStream_t) { return phase_halo(c, c->step); });
+        const int t_h = g->add("halo_force", 0, [c](cudaStream_t) { return phase_halo_force(c, c->step); });
         g->edge(t_force, t_h);
         g->edge(t_gx, t_h);
         last = t_h;
