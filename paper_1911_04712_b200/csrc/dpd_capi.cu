@@ -428,19 +428,25 @@ int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
 }
 
 // a7: boundary layers -> ghost messages.
-int phase_ghost_pack(dpd_ctx *c)
+int phase_ghost_pack(dpd_ctx *c, cudaStream_t st = nullptr)
 {
+    // reads only the sorted arrays and the cell starts, writes only the ghost messages and the
+    // boundary-cell list: in the step graph it runs on the communication stream, concurrently
+    // with the local forces
+    if (!st) st = c->stream;
     const Geom g = c->geom;
     const Msgs gs = c->gh.ms;
     CUDA_TRY(c, c->blist.reserve((size_t)g.ncell + 1));
-    CUDA_TRY(c, cudaMemsetAsync(c->blist.p, 0, sizeof(int), c->stream));
-    TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(gs); }));
+    CUDA_TRY(c, cudaMemsetAsync(c->blist.p, 0, sizeof(int), st));
+    TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, st>>>(gs); }, st));
     const dim3 grid((g.n[0] + kGpThreads - 1) / kGpThreads, g.n[1], g.n[2]);
-    return launch(c, KID_GHOST_PACK, [&] {
-        k_ghost_pack_cells<<<grid, kGpThreads, 0, c->stream>>>(c->pos[c->cur].p, c->vel[c->cur].p,
-                                                                        c->start[c->scur].p, g, gs, c->blist.p,
-                                                                        c->err.p);
-    });
+    return launch(
+        c, KID_GHOST_PACK,
+        [&] {
+            k_ghost_pack_cells<<<grid, kGpThreads, 0, st>>>(c->pos[c->cur].p, c->vel[c->cur].p, c->start[c->scur].p, g,
+                                                            gs, c->blist.p, c->err.p);
+        },
+        st);
 }
 
 // a5: local-local pairs at RNG step index `step`.
@@ -884,7 +890,7 @@ int dump_copyout(dpd_ctx *c, cudaStream_t st)
 
 // ---- one step of one context as a task graph (NCCL or single) ----------------------------
 // Tasks (stream slot): kick_drift_bin (0) -> [migrate_exchange (0)] -> scan_scatter (0) ->
-// [ghost_pack (0) -> ghost_exchange (1, comm stream) -> ghost_sort (1)] ; force_local (0) ->
+// [ghost_pack -> ghost_exchange -> ghost_sort (all 1, comm stream)] ; force_local (0) ->
 // [halo_force (0), after ghost_sort] -> [snapshot (0) -> snapshot_d2h (2, copy stream)].  Kahn's order
 // issues ghost_exchange before force_local, so the exchange overlaps the interior forces
 // (P:244-247); cross-stream edges become CUDA events.
@@ -910,7 +916,7 @@ dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
     g->edge(last, t_sort);
     int t_gx = -1;
     if (c->dist) {
-        const int t_gp = g->add("ghost_pack", 0, [c](cudaStream_t) { return phase_ghost_pack(c); });
+        const int t_gp = g->add("ghost_pack", 1, [c](cudaStream_t s) { return phase_ghost_pack(c, s); });
         g->edge(t_sort, t_gp);
         t_gx = g->add("ghost_exchange", 1, [c](cudaStream_t s) { return exchange_nccl(c, c->gh, s); });
         g->edge(t_gp, t_gx);
