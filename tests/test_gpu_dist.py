@@ -138,12 +138,14 @@ def test_group_temperature_and_momentum():
         destroy(capi, ctxs)
 
 
-def test_group_full_size_sampled_parity():
-    """2x2x2 group over BASELINE config 4's 128^3 box at rho = 8 (16.8 M particles, 64^3 per
-    subdomain as in bench's multi-GPU weak run): after the prime and 3 steps with migration,
-    sampled all-j force sums (local + halo pairs) against the oracle's plain definition (C-1),
-    every id present exactly once, sum F = 0."""
-    cfg = workloads.CONFIGS["weak128"]
+@pytest.mark.parametrize("name", ["weak128", "strong256"])
+def test_group_full_size_sampled_parity(name):
+    """2x2x2 group over BASELINE config 4's 128^3 box (16.8 M particles, 64^3 per subdomain)
+    and config 5's 256^3 box (134 M particles, 128^3 per subdomain: the weak-scaling subdomain
+    of the multi-GPU bench) at rho = 8: after the prime and 3 steps with migration, sampled
+    all-j force sums (local + halo pairs) against the oracle's plain definition (C-1), every id
+    present exactly once, sum F = 0."""
+    cfg = workloads.CONFIGS[name]
     p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
                          seed=cfg.seed)
     pos0, vel0 = workloads.make_config(cfg)
@@ -161,7 +163,8 @@ def test_group_full_size_sampled_parity():
         assert pos.shape[0] == n and np.array_equal(np.sort(ids), ids0)
         # boundary particles sit in the halo of up to 7 other subdomains: sample those too
         rng = np.random.default_rng(7)
-        near = np.where(np.any(np.abs(np.mod(pos, 64.0) - 32.0) > 31.0, axis=1))[0]
+        half = cfg.box[0] / 2.0  # subdomain edge
+        near = np.where(np.any(np.abs(np.mod(pos, half) - half / 2.0) > half / 2.0 - 1.0, axis=1))[0]
         sel = np.concatenate([rng.choice(n, 16, replace=False), rng.choice(near, 16, replace=False)])
         F_ref, allow = oracle.forces_subset(p, pos, u, steps.pop(), sel, ids=ids.astype(np.uint32),
                                             eps=boundary_eps(cfg.box))
