@@ -121,7 +121,7 @@ class ClockSampler:
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device_index=0, period=0.05):
+    def __init__(self, device_index=0, period=0.01):
         self.samples = []
         self.reasons = 0
         self.period = period
