@@ -2087,16 +2087,21 @@ int dpd_get_forces_ex(dpd_ctx *c, int64_t cap, float *f, int32_t *ids, int64_t *
 }
 
 // ---- NEXT-4: asynchronous dumps, step schedule, task graph and I/O queue (host) ----------
-int dpd_dump_open(dpd_ctx *c, const char *path_prefix, int queue_depth)
+// Device / pinned resources of a dump state (its writer already closed).
+static void dump_free(DumpState *d)
 {
-    if (!c || !path_prefix) return DPD_ERR_ARG;
-    if (queue_depth < 0 || queue_depth > 64) return fail(c, DPD_ERR_ARG, "queue_depth must be in [0, 64]");
-    if (c->dump) return fail(c, DPD_ERR_ARG, "dumps already open; dpd_dump_close first");
-    auto *d = new DumpState();
-    d->prefix = path_prefix;
-    d->depth = queue_depth;
-    cudaGetDevice(&d->device);
-    d->slots.resize(queue_depth + 1);
+    for (auto &sl : d->slots) {
+        if (sl.host) cudaFreeHost(sl.host);
+        if (sl.copied) cudaEventDestroy(sl.copied);
+    }
+    if (d->staged_free) cudaEventDestroy(d->staged_free);
+    if (d->dev) cudaFree(d->dev);
+    delete d->q;
+    delete d;
+}
+
+static int dump_setup(dpd_ctx *c, DumpState *d)
+{
     for (auto &sl : d->slots) CUDA_TRY(c, cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&d->staged_free, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventRecord(d->staged_free, c->stream));
@@ -2107,6 +2112,24 @@ int dpd_dump_open(dpd_ctx *c, const char *path_prefix, int queue_depth)
         d->cap = c->n_cap;
         CUDA_TRY(c, cudaMalloc(&d->dev, dump_bytes(d->cap)));
         for (auto &sl : d->slots) CUDA_TRY(c, cudaMallocHost(&sl.host, dump_bytes(d->cap)));
+    }
+    return DPD_OK;
+}
+
+int dpd_dump_open(dpd_ctx *c, const char *path_prefix, int queue_depth)
+{
+    if (!c || !path_prefix) return DPD_ERR_ARG;
+    if (queue_depth < 0 || queue_depth > 64) return fail(c, DPD_ERR_ARG, "queue_depth must be in [0, 64]");
+    if (c->dump) return fail(c, DPD_ERR_ARG, "dumps already open; dpd_dump_close first");
+    auto *d = new DumpState();
+    d->prefix = path_prefix;
+    d->depth = queue_depth;
+    cudaGetDevice(&d->device);
+    d->slots.resize(queue_depth + 1);
+    const int rc = dump_setup(c, d);
+    if (rc != DPD_OK) {
+        dump_free(d); // nothing was queued: no writer yet
+        return rc;
     }
     d->q = new dpd::IoQueue(queue_depth);
     c->dump = d;
@@ -2141,15 +2164,8 @@ int dpd_dump_close(dpd_ctx *c, int64_t *written)
     std::string err;
     const int rc = d->q->close(&err);
     if (written) *written = d->q->completed();
-    delete d->q;
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-    for (auto &sl : d->slots) {
-        if (sl.host) cudaFreeHost(sl.host);
-        if (sl.copied) cudaEventDestroy(sl.copied);
-    }
-    if (d->staged_free) cudaEventDestroy(d->staged_free);
-    if (d->dev) cudaFree(d->dev);
-    delete d;
+    dump_free(d);
     c->dump = nullptr;
     delete c->step_graph[1]; // the snapshot tasks refer to the closed state
     c->step_graph[1] = nullptr;
