@@ -265,6 +265,7 @@ __device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, 
 // phases.  One-sided (C-19): the
 // i-side sums go to fixed-point shared accumulators, then once to frc.
 constexpr int kHcWarps = 4;
+constexpr int kHcI = 4; // local particles tested per candidate round
 
 template <int KMODE>
 __global__ void __launch_bounds__(32 * kHcWarps)
@@ -274,7 +275,8 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                        const int *__restrict__ gstart, Geom g, PairP pp, float scale, float inv_scale,
                        uint32_t s_lo, uint32_t s_hi)
 {
-    __shared__ unsigned qbuf[kHcWarps][96]; // < 32 pending + 2 x 32 new
+    __shared__ unsigned qbuf[kHcWarps][32 + 32 * kHcI]; // < 32 pending + kHcI x 32 new
+    __shared__ float4 spi[kHcWarps][32];                // the cell's local positions (broadcast reads)
     __shared__ int acc[kHcWarps][3][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned *q = qbuf[warp];
@@ -312,6 +314,7 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                 vi = vel[s0 + ib + lane];
             }
             acc[warp][0][lane] = acc[warp][1][lane] = acc[warp][2][lane] = 0;
+            spi[warp][lane] = pi;
             __syncwarp();
             int qn = 0;
             // evaluate queue entries [0, cnt): lane k takes entry k
@@ -362,22 +365,23 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                     pz = pj.z + shz;
                 }
                 const unsigned tag = jidx | ((unsigned)d << 27);
-                for (int ii = 0; ii < ni; ii += 2) { // two local particles per round
-                    const int i1 = min(ii + 1, 31);
-                    const float ax = __shfl_sync(0xffffffffu, pi.x, ii) - px;
-                    const float ay = __shfl_sync(0xffffffffu, pi.y, ii) - py;
-                    const float az = __shfl_sync(0xffffffffu, pi.z, ii) - pz;
-                    const float bx = __shfl_sync(0xffffffffu, pi.x, i1) - px;
-                    const float by = __shfl_sync(0xffffffffu, pi.y, i1) - py;
-                    const float bz = __shfl_sync(0xffffffffu, pi.z, i1) - pz;
-                    const float ra = ax * ax + ay * ay + az * az, rb = bx * bx + by * by + bz * bz;
-                    const bool ha = ra < pp.rc2 && ra > 0.0f;
-                    const bool hb = ii + 1 < ni && rb < pp.rc2 && rb > 0.0f;
-                    const unsigned ma = __ballot_sync(0xffffffffu, ha), mb = __ballot_sync(0xffffffffu, hb);
+                for (int ii = 0; ii < ni; ii += kHcI) { // kHcI local particles per round
+                    unsigned m[kHcI];
+                    bool h[kHcI];
+#pragma unroll
+                    for (int u = 0; u < kHcI; ++u) {
+                        const float4 p = spi[warp][min(ii + u, 31)]; // LDS.128 broadcast
+                        const float rx = p.x - px, ry = p.y - py, rz = p.z - pz;
+                        const float r2 = rx * rx + ry * ry + rz * rz;
+                        h[u] = ii + u < ni && r2 < pp.rc2 && r2 > 0.0f;
+                        m[u] = __ballot_sync(0xffffffffu, h[u]);
+                    }
                     const unsigned lt = lanemask_lt();
-                    if (ha) q[qn + __popc(ma & lt)] = tag | ((unsigned)ii << 22);
-                    if (hb) q[qn + __popc(ma) + __popc(mb & lt)] = tag | ((unsigned)(ii + 1) << 22);
-                    qn += __popc(ma) + __popc(mb);
+#pragma unroll
+                    for (int u = 0; u < kHcI; ++u) {
+                        if (h[u]) q[qn + __popc(m[u] & lt)] = tag | ((unsigned)(ii + u) << 22);
+                        qn += __popc(m[u]);
+                    }
                     __syncwarp();
                     while (qn >= 32) {
                         evaluate(32);
