@@ -218,6 +218,30 @@ def run_reference(args, cfg):
     return 0
 
 
+def rank_boxes(cfg, world, scaling):
+    """(global box, subdomain) of an N-GPU run: weak = the config's box per GPU, strong = the
+    config's box split over the GPUs (rank grid as rank_grid)."""
+    grid = rank_grid(world)
+    gbox = tuple(cfg.box[k] if scaling == "strong" else cfg.box[k] * grid[k] for k in range(3))
+    return gbox, tuple(gbox[k] / grid[k] for k in range(3))
+
+
+def rank_particles(cfg, world, rank, scaling="weak"):
+    """This rank's own particles (global coordinates inside its subdomain, float32), velocities
+    and globally unique ids; rank -> subdomain coordinates as the library's (x fastest)."""
+    grid = rank_grid(world)
+    sub = rank_boxes(cfg, world, scaling)[1]
+    coord = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
+    pos, vel = workloads.make_particles(sub, cfg.rho, cfg.kT, init_seed=1 + rank)
+    pos = (pos + np.array([coord[k] * sub[k] for k in range(3)], np.float32)).astype(np.float32)
+    for k in range(3):  # the shift can round up onto the next subdomain's face: keep it local
+        hi = np.float32((coord[k] + 1) * sub[k])
+        pos[pos[:, k] >= hi, k] = np.nextafter(hi, np.float32(0.0))
+    n_local = pos.shape[0]
+    ids = (np.arange(n_local, dtype=np.int64) + rank * n_local).astype(np.int32)
+    return pos, vel, ids, coord, sub
+
+
 def config_block(cfg, args, world):
     g = rank_grid(world)
     strong = getattr(args, "scaling", "weak") == "strong"
@@ -265,9 +289,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     grid = rank_grid(world)
-    strong = args.scaling == "strong"
-    gbox = tuple(cfg.box[k] if strong else cfg.box[k] * grid[k] for k in range(3))
-    sub = tuple(gbox[k] / grid[k] for k in range(3))  # this rank's subdomain
+    gbox = rank_boxes(cfg, world, args.scaling)[0]
     stream = torch.cuda.Stream()
 
     # --- build the context and the workload -------------------------------------------------
@@ -294,15 +316,8 @@ def main():
         capi.dpd_set_option(ctx, name, int(val))
     if cfg.body_f:
         capi.dpd_set_body_force(ctx, cfg.body_f)
-    # each rank generates only its own subdomain's particles with globally unique ids
-    coord = (rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1]))
-    pos, vel = workloads.make_particles(sub, cfg.rho, cfg.kT, init_seed=1 + rank)
-    pos = (pos + np.array([coord[k] * sub[k] for k in range(3)], np.float32)).astype(np.float32)
-    for k in range(3):  # the shift can round up onto the next subdomain's face: keep it local
-        hi = np.float32((coord[k] + 1) * sub[k])
-        pos[pos[:, k] >= hi, k] = np.nextafter(hi, np.float32(0.0))
+    pos, vel, ids = rank_particles(cfg, world, rank, args.scaling)[:3]
     n_local = pos.shape[0]
-    ids = (np.arange(n_local, dtype=np.int64) + rank * n_local).astype(np.int32)
     pos_h = torch.from_numpy(pos).pin_memory()
     vel_h = torch.from_numpy(vel).pin_memory()
     ids_h = torch.from_numpy(ids).pin_memory()
