@@ -174,3 +174,23 @@ def test_group_full_size_sampled_parity(name):
         assert np.abs(f.astype(np.float64).sum(0)).max() < 1e-5 * np.abs(f).sum()
     finally:
         destroy(capi, ctxs)
+
+
+def test_ghost_capacity_overflow_is_reported():
+    """Message slots sized far below the boundary-layer occupancy (message_capacity_percent =
+    10): the ghost pack counts the overflow, writes only what fits and the step reports
+    DPD_ERR_CAPACITY instead of corrupting memory."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
+    pos0, vel0 = workloads.make_config(cfg)
+    _, ctxs = make_group(cfg, (2, 1, 1))
+    try:
+        ids0 = np.arange(pos0.shape[0], dtype=np.int32)
+        for c in ctxs:
+            capi.dpd_set_option(c, "message_capacity_percent", 10)
+            capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
+        with pytest.raises(capi.DPDError) as e:
+            capi.dpd_group_step(ctxs, 1)
+        assert e.value.code == capi.DPD_ERR_CAPACITY
+    finally:
+        destroy(capi, ctxs)
