@@ -194,3 +194,35 @@ def test_ghost_capacity_overflow_is_reported():
         assert e.value.code == capi.DPD_ERR_CAPACITY
     finally:
         destroy(capi, ctxs)
+
+
+def test_group_empty_and_one_sided_sets():
+    """Edge cases of the decomposition: an empty set (n = 0) steps without work on every
+    member, and a set living entirely inside one subdomain leaves the others empty but still
+    exchanging (zero-count messages) while it expands into them."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
+    _, ctxs = make_group(cfg, (2, 2, 1))
+    try:
+        e = np.zeros((0, 3), np.float32)
+        for c in ctxs:
+            capi.dpd_set_particles_ex(c, e, e, np.zeros(0, np.int32), 0)
+        capi.dpd_group_step(ctxs, 5)
+        assert [capi.dpd_get_count(c) for c in ctxs] == [0, 0, 0, 0]
+        pos0, vel0 = workloads.make_config(cfg)
+        inside = np.all(pos0 < 5.5, axis=1)  # all in member 0's subdomain [0, 6)^2 x [0, 12)
+        pos1, vel1 = pos0[inside], vel0[inside]  # the block expands into the empty members
+        ids1 = np.arange(pos1.shape[0], dtype=np.int32)
+        for c in ctxs:
+            # message slots are sized from the global density (here ~1/5 of member 0's):
+            # a non-uniform set needs the documented head-room option
+            capi.dpd_set_option(c, "message_capacity_percent", 800)
+            capi.dpd_set_particles_ex(c, pos1, vel1, ids1, 0)
+        assert [capi.dpd_get_count(c) for c in ctxs][1:] == [0, 0, 0]
+        capi.dpd_group_step(ctxs, 100)
+        counts = [capi.dpd_get_count(c) for c in ctxs]
+        assert sum(counts) == pos1.shape[0] and min(counts[1:]) > 0
+        ids = np.concatenate([gather_state(capi, [c])[3] for c in ctxs])
+        assert np.array_equal(np.sort(ids), ids1)
+    finally:
+        destroy(capi, ctxs)
