@@ -79,7 +79,10 @@ int dpd_set_stream(dpd_ctx *ctx, void *cuda_stream);
  *                  variant of the tiled kernel (one warp per home cell; same results up
  *                  to fp32 summation order).  1 and 2 are single-domain only.
  *   "message_capacity_percent" (distributed contexts) scales the per-direction message
- *                  capacities (default 100; >= 10).
+ *                  capacities (default 100; >= 10).  Capacities follow the set's global mean
+ *                  density; a strongly non-uniform set (a dense block in an empty box) needs
+ *                  head-room here, else the step returns DPD_ERR_CAPACITY (nothing is written
+ *                  past a slot).
  *   "tile_persistent" 1 = run the tiled kernel as resident CTAs walking the tiles (the next
  *                  tile's cell table and staging overlap the current tile's pairs / flush);
  *                  0 = one CTA per tile (default, measured faster: DESIGN.md §6).
