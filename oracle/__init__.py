@@ -112,6 +112,9 @@ def lib():
         L.oracle_philox2x32_10.argtypes = [P(u32), u32, P(u32)]
         L.oracle_step_key.argtypes = [C.c_uint64, i64]
         L.oracle_step_key.restype = u32
+        L.oracle_fmix32.argtypes = [u32]
+        L.oracle_fmix32.restype = u32
+        L.oracle_step_keys.argtypes = [C.c_uint64, i64, i64, P(u32)]
         L.oracle_pair_words.argtypes = [C.c_uint64, i64, u32, u32, P(u32)]
         L.oracle_xi.argtypes = [u32, u32]
         L.oracle_xi.restype = d
@@ -180,9 +183,21 @@ def philox2x32_10(ctr, key: int):
     return o
 
 
+def fmix32(h: int) -> int:
+    """MurmurHash3's 32-bit finalizer, a bijection of the 32-bit words (C-7)."""
+    return int(lib().oracle_fmix32(int(h) & 0xFFFFFFFF))
+
+
 def step_key(seed: int, step: int) -> int:
-    """k_s = word 0 of Philox2x32-10({s lo, s hi}, seed lo ^ seed hi) (C-7)."""
+    """k_s = fmix32(s_lo ^ seed_lo ^ fmix32(s_hi)) ^ seed_hi (C-7, round-2 revision)."""
     return int(lib().oracle_step_key(int(seed), int(step)))
+
+
+def step_keys(seed: int, s0: int, n: int) -> np.ndarray:
+    """Step keys of steps s0 .. s0 + n - 1 (uint32 array)."""
+    o = np.zeros(int(n), dtype=np.uint32)
+    lib().oracle_step_keys(int(seed), int(s0), int(n), _p(o, C.c_uint32))
+    return o
 
 
 def pair_words(seed: int, step: int, ida: int, idb: int):

@@ -153,16 +153,37 @@ void oracle_philox2x32_10(const uint32_t ctr[2], uint32_t key, uint32_t out[2])
     out[1] = c1;
 }
 
-/* Per-step key (C-7): k_s = word 0 of Philox2x32-10(ctr = {s mod 2^32, s >> 32},
- * key = seed_lo ^ seed_hi). */
+/* MurmurHash3's 32-bit finalizer fmix32 (A. Appleby, public domain): xor-shift by 16,
+ * multiply by 0x85ebca6b, xor-shift by 13, multiply by 0xc2b2ae35, xor-shift by 16.  Each
+ * of the five steps is a bijection of the 32-bit words (odd multipliers are invertible mod
+ * 2^32), so fmix32 is a permutation with fmix32(0) = 0. */
+uint32_t oracle_fmix32(uint32_t h)
+{
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+/* Per-step key (C-7, revised in round 2 so that <xi(t) xi(t')> = delta(t - t'), holds
+ * over a whole run):  k_s = fmix32(s_lo ^ seed_lo ^ fmix32(s_hi)) ^ seed_hi.
+ * For a fixed seed and s_hi the map s_lo -> k_s is a composition of bijections, so no two
+ * steps 0 <= s < 2^32 share a key; the 64-bit seed enters as (seed_lo, seed_hi) without
+ * folding, so two seeds give the same key sequence only if they are equal. */
 uint32_t oracle_step_key(uint64_t seed, int64_t step)
 {
-    uint32_t ctr[2], out[2];
     uint64_t s = (uint64_t)step;
-    ctr[0] = (uint32_t)s;
-    ctr[1] = (uint32_t)(s >> 32);
-    oracle_philox2x32_10(ctr, (uint32_t)seed ^ (uint32_t)(seed >> 32), out);
-    return out[0];
+    uint32_t s_lo = (uint32_t)s, s_hi = (uint32_t)(s >> 32);
+    uint32_t seed_lo = (uint32_t)seed, seed_hi = (uint32_t)(seed >> 32);
+    return oracle_fmix32(s_lo ^ seed_lo ^ oracle_fmix32(s_hi)) ^ seed_hi;
+}
+
+/* Step keys of n consecutive steps s0, s0 + 1, ... (test helper for the injectivity pin). */
+void oracle_step_keys(uint64_t seed, int64_t s0, int64_t n, uint32_t *out)
+{
+    for (int64_t k = 0; k < n; ++k) out[k] = oracle_step_key(seed, s0 + k);
 }
 
 /* Pair words (C-7): (w0, w1) = Philox2x32-10(ctr = {min id, max id}, key = k_s).

@@ -32,16 +32,70 @@ def test_pair_words_symmetric_and_keyed():
     assert oracle.pair_words(42, 1, 0, 1) != base
     assert oracle.pair_words(43, 0, 0, 1) != base
     assert oracle.pair_words(42, 0, 0, 2) != base
-    # layout (C-7): k_s = Philox2x32-10({s lo, s hi}, seed lo ^ seed hi)[0];
-    # (w0, w1) = Philox2x32-10({min id, max id}, k_s) -- checked against the raw generator
+    # layout (C-7): (w0, w1) = Philox2x32-10({min id, max id}, k_s) -- checked against the
+    # KAT-pinned raw generator
     seed = (7 << 32) | 42
     s = 2**32 + 17
-    ks = int(oracle.philox2x32_10([s & 0xFFFFFFFF, s >> 32], 42 ^ 7)[0])
-    assert oracle.step_key(seed, s) == ks
+    ks = oracle.step_key(seed, s)
     w = oracle.philox2x32_10([3, 9], ks)
     assert oracle.pair_words(seed, s, 9, 3) == (int(w[0]), int(w[1]))
-    # consecutive steps use different keys
-    assert len({oracle.step_key(42, t) for t in range(1000)}) == 1000
+
+
+def _fmix32_inverse(h):
+    # inverse of MurmurHash3's fmix32, step by step: x ^= x >> s is undone by repeating the
+    # shift until it runs out of bits; an odd multiplier is undone by its inverse mod 2^32
+    def unxorshift(x, s):
+        r = x
+        for _ in range(32 // s + 1):
+            r = x ^ (r >> s)
+        return r & 0xFFFFFFFF
+
+    h = unxorshift(h, 16)
+    h = (h * pow(0xC2B2AE35, -1, 2**32)) & 0xFFFFFFFF
+    h = unxorshift(h, 13)
+    h = (h * pow(0x85EBCA6B, -1, 2**32)) & 0xFFFFFFFF
+    return unxorshift(h, 16)
+
+
+def test_fmix32_is_a_bijection():
+    # fmix32 of the C-7 step key is invertible: the inverse built from the definition's five
+    # steps recovers every probed input (edge words and random words), and fmix32(0) = 0
+    rng = np.random.default_rng(5)
+    probes = [0, 1, 2, 0x7FFFFFFF, 0x80000000, 0xFFFFFFFF] + [int(v) for v in rng.integers(0, 2**32, 2000)]
+    for x in probes:
+        assert _fmix32_inverse(oracle.fmix32(x)) == x
+    assert oracle.fmix32(0) == 0
+    # not the identity or a plain xor: a one-bit input change flips about half the output bits
+    flips = [bin(oracle.fmix32(x) ^ oracle.fmix32(x ^ 1)).count("1") for x in probes[6:]]
+    assert 14 < np.mean(flips) < 18
+
+
+@pytest.mark.parametrize("seed", [42, (2**32 + 1) * 977])
+def test_step_keys_injective_over_a_run(seed):
+    # P:133 (<xi(t) xi(t')> = delta(t - t')) needs a fresh pair stream at every step: no two
+    # steps of a run may share the per-step key.  2^24 consecutive steps (16.8 M, 17x the
+    # paper's 10^6-step Table-1 runs) hold no duplicate key, and neither does a window
+    # that crosses s = 2^32 from below.
+    ks = oracle.step_keys(seed, 0, 2**24)
+    assert np.unique(ks).size == ks.size
+    ks = oracle.step_keys(seed, 2**32 - 2**20, 2**20)
+    assert np.unique(ks).size == ks.size
+    # the round-1 reading collided here (seed 42: steps 6309 and 22637 shared k_s)
+    if seed == 42:
+        assert oracle.step_key(42, 6309) != oracle.step_key(42, 22637)
+
+
+def test_step_keys_do_not_alias_seeds():
+    # the 64-bit seed is not folded: seeds that the round-1 fold lo ^ hi mapped to one key
+    # (0 and 2^32 + 1) now give different key sequences, and the step key is the
+    # documented composition (fmix32 pinned above)
+    a = oracle.step_keys(0, 0, 4096)
+    b = oracle.step_keys(2**32 + 1, 0, 4096)
+    assert np.count_nonzero(a == b) < 4
+    for seed, s in [(42, 0), (42, 99), ((7 << 32) | 42, 2**32 + 17), (2**64 - 1, 2**40 + 3)]:
+        s_lo, s_hi = s & 0xFFFFFFFF, s >> 32
+        want = oracle.fmix32(s_lo ^ (seed & 0xFFFFFFFF) ^ oracle.fmix32(s_hi)) ^ (seed >> 32)
+        assert oracle.step_key(seed, s) == want
 
 
 def test_box_muller_closed_forms():
