@@ -15,7 +15,8 @@
  *     F^R = sigma xi_ij w_R e / sqrt(dt);  w_R = w^k, w_D = w_R^2,
  *     sigma^2 = 2 gamma kT                                               (C-3, C-4)
  *   - xi_ij by Box-Muller on (w0, w1) = Philox2x32-10(ctr = {min id, max id}, key = k_s),
- *     k_s = word 0 of Philox2x32-10({step lo, step hi}, seed lo ^ seed hi) (C-7)
+ *     k_s = fmix32(step_lo ^ seed_lo ^ fmix32(step_hi)) ^ seed_hi, a bijection of step_lo
+ *     (no two steps below 2^32 share a key; fmix32 = MurmurHash3's finalizer) (C-7)
  *   - cell lists of edge >= r_c rebuilt every step
  *   - "fused Velocity-Verlet" = Groot-Warren VV, lambda = 1/2             (C-6)
  *   - 3D domain decomposition with ghost exchange and redistribution
@@ -56,7 +57,7 @@ enum {
  *   kT      : temperature (>= 0); sigma = sqrt(2 gamma kT) is derived
  *   power   : kernel exponent k in (0, 1]; w_R = w^k                          P:136, C-4
  *   dt      : time step (> 0)
- *   seed    : 64-bit Philox key of the pair RNG                               C-7
+ *   seed    : 64-bit seed of the pair RNG (enters the per-step key unfolded)   C-7
  *   out     : receives the new context (NULL on failure)
  * Returns DPD_OK, DPD_ERR_ARG (out == NULL), DPD_ERR_CONFIG or DPD_ERR_CUDA. */
 int dpd_create(const double box[3], double rc, double a, double gamma, double kT,

@@ -450,20 +450,13 @@ int phase_ghost_pack(dpd_ctx *c, cudaStream_t st = nullptr)
 }
 
 // a5: local-local pairs at RNG step index `step`.
-// Host Philox2x32-10 (C-7) for the per-step key: k_s = word 0 of
-// Philox2x32-10({s lo, s hi}, seed lo ^ seed hi); the tiled kernel receives the ten round
-// keys k_s + r W as a parameter (dpd_device.cuh RoundKeys).
-RoundKeys host_round_keys(uint32_t s_lo, uint32_t s_hi, uint32_t seed_fold)
+// Per-step key on the host (C-7): k_s = fmix32(s_lo ^ seed_lo ^ fmix32(s_hi)) ^ seed_hi; the
+// tiled kernel receives the ten round keys k_s + r W as a parameter (dpd_device.cuh RoundKeys).
+RoundKeys host_round_keys(uint32_t s_lo, uint32_t s_hi, const PairP &pp)
 {
-    uint32_t c0 = s_lo, c1 = s_hi, k = seed_fold;
-    for (int r = 0; r < 10; ++r) {
-        const uint64_t prod = (uint64_t)kPhilox2M * c0;
-        c0 = (uint32_t)(prod >> 32) ^ k ^ c1;
-        c1 = (uint32_t)prod;
-        k += kPhilox2W;
-    }
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_lo, pp.seed_hi);
     RoundKeys K;
-    for (int r = 0; r < 10; ++r) K.k[r] = c0 + (uint32_t)r * kPhilox2W;
+    for (int r = 0; r < 10; ++r) K.k[r] = ks + (uint32_t)r * kPhilox2W;
     return K;
 }
 
@@ -519,7 +512,7 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
         // by the power-of-two scale (exact), so one FFMA per component quantises
         const PairP pp = scaled_pair(c->pp, fx.scale);
-        const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp.seed_fold);
+        const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp);
         const dim3 tgrid((g.n[0] + FT_BX - 1) / FT_BX, (g.n[1] + FT_BY - 1) / FT_BY, (g.n[2] + FT_BZ - 1) / FT_BZ);
         const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
                           ((g.n[2] + FT_BZ - 1) / FT_BZ);
@@ -1112,7 +1105,8 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     pp.inv_rc = (float)(1.0 / rc);
     pp.rc2 = (float)(rc * rc);
     pp.power = (float)power;
-    pp.seed_fold = (uint32_t)seed ^ (uint32_t)(seed >> 32);
+    pp.seed_lo = (uint32_t)seed;
+    pp.seed_hi = (uint32_t)(seed >> 32);
     c->pp = pp;
     set_fixed_scale(c, a, gamma);
     c->fix.prune = 1;
@@ -1905,7 +1899,7 @@ int dpd_debug_pair_words(int64_t n, const uint32_t *quad_in, uint64_t seed, uint
     cudaMalloc(&dw, sizeof(uint2) * n);
     cudaMalloc(&dxi, sizeof(float) * n);
     cudaMemcpy(din, quad_in, sizeof(uint4) * n, cudaMemcpyHostToDevice);
-    k_pair_words<<<nblk(n, 128), 128>>>(din, (uint32_t)seed ^ (uint32_t)(seed >> 32), dxi, dw, (int)n);
+    k_pair_words<<<nblk(n, 128), 128>>>(din, (uint32_t)seed, (uint32_t)(seed >> 32), dxi, dw, (int)n);
     cudaMemcpy(words, dw, sizeof(uint2) * n, cudaMemcpyDeviceToHost);
     cudaError_t e = cudaMemcpy(xi, dxi, sizeof(float) * n, cudaMemcpyDeviceToHost);
     cudaFree(din);

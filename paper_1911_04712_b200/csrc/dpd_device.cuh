@@ -36,7 +36,7 @@ struct PairP {
     float inv_rc;   // 1 / r_c
     float rc2;      // r_c^2
     float power;    // k (w_R = w^k)                                         (C-4)
-    uint32_t seed_fold; // seed lo ^ seed hi: key of the per-step key          (C-7)
+    uint32_t seed_lo, seed_hi; // the 64-bit seed, unfolded: per-step key       (C-7)
     // NEXT-2 species matrix (KMODE == 3 only): entry ti * DPD_MAX_SPECIES + tj holds the
     // pair's a, gamma and sigma/sqrt(dt); ti, tj travel in vel.w
     float sa[DPD_MAX_SPECIES * DPD_MAX_SPECIES];
@@ -64,8 +64,9 @@ struct IntegP {
 
 // ---------------------------------------------------------------------------------------
 // Pair RNG (C-7): Philox2x32-10 (Random123).  Round: (hi, lo) = M * c0;
-// c' = (hi ^ k ^ c1, lo); k += W.  Per-step key k_s = Philox2x32-10({s lo, s hi},
-// seed lo ^ seed hi)[0]; pair words (w0, w1) = Philox2x32-10({min id, max id}, k_s).
+// c' = (hi ^ k ^ c1, lo); k += W.  Per-step key k_s = fmix32(s_lo ^ seed_lo ^ fmix32(s_hi))
+// ^ seed_hi (a bijection of s_lo: no two steps below 2^32 share a key); pair words
+// (w0, w1) = Philox2x32-10({min id, max id}, k_s).
 // ---------------------------------------------------------------------------------------
 constexpr uint32_t kPhilox2M = 0xD256D193u;
 constexpr uint32_t kPhilox2W = 0x9E3779B9u;
@@ -82,9 +83,21 @@ __device__ __forceinline__ uint2 philox2x32_10(uint32_t c0, uint32_t c1, uint32_
     return make_uint2(c0, c1);
 }
 
-__device__ __forceinline__ uint32_t step_key(uint32_t s_lo, uint32_t s_hi, uint32_t seed_fold)
+// MurmurHash3's 32-bit finalizer: five bijective steps (xor-shifts, odd multipliers).
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h)
 {
-    return philox2x32_10(s_lo, s_hi, seed_fold).x;
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+__host__ __device__ __forceinline__ uint32_t step_key(uint32_t s_lo, uint32_t s_hi, uint32_t seed_lo,
+                                                      uint32_t seed_hi)
+{
+    return fmix32(s_lo ^ seed_lo ^ fmix32(s_hi)) ^ seed_hi;
 }
 
 // Words (w0, w1) of the pair (ida, idb) under the per-step key ks.

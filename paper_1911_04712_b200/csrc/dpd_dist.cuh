@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(32 * kHcWarps)
     __shared__ int acc[kHcWarps][3][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned *q = qbuf[warp];
-    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_lo, pp.seed_hi);
     const int nbc = bcells[0];
     for (int w = blockIdx.x * kHcWarps + warp; w < nbc; w += gridDim.x * kHcWarps) {
         const int gc = bcells[1 + w];

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(FC_NTHR, 3)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ForceCellSmem &S = *reinterpret_cast<ForceCellSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_lo, pp.seed_hi);
 
     // ---- tile geometry: every thread decodes blockIdx ----------------------------------
     const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;

@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(128) k_force_ref(const float4 *__restrict__ po
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_fold);
+    const uint32_t ks = step_key(s_lo, s_hi, pp.seed_lo, pp.seed_hi);
     const float4 pi = pos[i], vi = vel[i];
     const uint32_t idi = (uint32_t)__float_as_int(pi.w);
     const int cx = cell_coord(pi.x, g.inv_h[0], g.n[0]);
@@ -710,13 +710,13 @@ __global__ void k_philox2(const uint2 *__restrict__ ctr, const uint32_t *__restr
     if (i < n) out[i] = philox2x32_10(ctr[i].x, ctr[i].y, key[i]);
 }
 
-__global__ void k_pair_words(const uint4 *__restrict__ in, uint32_t seed_fold, float *__restrict__ xi,
+__global__ void k_pair_words(const uint4 *__restrict__ in, uint32_t seed_lo, uint32_t seed_hi, float *__restrict__ xi,
                              uint2 *__restrict__ w, int n)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint4 q = in[i]; // ida, idb, s_lo, s_hi
-    const uint2 wd = pair_words(q.x, q.y, step_key(q.z, q.w, seed_fold));
+    const uint2 wd = pair_words(q.x, q.y, step_key(q.z, q.w, seed_lo, seed_hi));
     w[i] = wd;
     xi[i] = box_muller(wd.x, wd.y);
 }
