@@ -121,9 +121,9 @@ def lib():
         L.oracle_pair_force.argtypes = [P(Params), dp, dp, u32, u32, i64, dp, dp]
         L.oracle_pair_force.restype = C.c_int
         L.oracle_min_image.argtypes = [P(Params), dp, dp, dp]
-        L.oracle_forces.argtypes = [P(Params), i64, dp, dp, P(u32), i64, d, dp, dp, P(i64)]
-        L.oracle_forces_subset.argtypes = [P(Params), i64, dp, dp, P(u32), i64, d, i64, P(i64), dp, dp]
-        L.oracle_pairs.argtypes =[P(Params), i64, dp, P(u32), i64, d, i64, P(u32), P(C.c_uint8)]
+        L.oracle_forces.argtypes = [P(Params), i64, dp, dp, P(u32), i64, d, d, dp, dp, P(i64)]
+        L.oracle_forces_subset.argtypes = [P(Params), i64, dp, dp, P(u32), i64, d, d, i64, P(i64), dp, dp]
+        L.oracle_pairs.argtypes = [P(Params), i64, dp, P(u32), i64, d, d, i64, P(u32), P(C.c_uint8)]
         L.oracle_pairs.restype = i64
         L.oracle_grid_dims.argtypes = [P(Params), P(C.c_int32)]
         L.oracle_cells.argtypes = [P(Params), i64, P(C.c_float), P(C.c_int32), P(C.c_int32), P(C.c_int32)]
@@ -231,9 +231,11 @@ def min_image(p: DPDParams, xi_, xj_):
     return d
 
 
-def forces(p: DPDParams, x, v, step: int, ids=None, eps: float = 0.0):
+def forces(p: DPDParams, x, v, step: int, ids=None, eps: float = 0.0, eps_image=None):
     """PairForces(x, v, s): O(N^2) minimum-image sum (C-1, C-2 item 4).
-    Returns (F[n,3], allow[n], npairs); allow = boundary-pair allowance (C-12)."""
+    Returns (F[n,3], allow[n], npairs); allow = boundary-pair allowance (C-12) over pairs
+    within eps of r_c (eps_image, default eps, for pairs across a periodic edge)."""
+    eps_image = eps if eps_image is None else eps_image
     x, v = _f64(x), _f64(v)
     n = x.shape[0]
     ids = _ids(n, ids)
@@ -242,13 +244,14 @@ def forces(p: DPDParams, x, v, step: int, ids=None, eps: float = 0.0):
     npairs = C.c_int64(0)
     pc = p.c()
     lib().oracle_forces(C.byref(pc), n, _p(x, C.c_double), _p(v, C.c_double), _p(ids, C.c_uint32),
-                        int(step), float(eps), _p(F, C.c_double), _p(allow, C.c_double),
+                        int(step), float(eps), float(eps_image), _p(F, C.c_double), _p(allow, C.c_double),
                         C.byref(npairs))
     return F, allow, int(npairs.value)
 
 
-def forces_subset(p: DPDParams, x, v, step: int, sel, ids=None, eps: float = 0.0):
+def forces_subset(p: DPDParams, x, v, step: int, sel, ids=None, eps: float = 0.0, eps_image=None):
     """PairForces for the selected particles only (same all-j sum).  Returns (F[m,3], allow[m])."""
+    eps_image = eps if eps_image is None else eps_image
     x, v = _f64(x), _f64(v)
     n = x.shape[0]
     ids = _ids(n, ids)
@@ -258,7 +261,7 @@ def forces_subset(p: DPDParams, x, v, step: int, sel, ids=None, eps: float = 0.0
     allow = np.zeros(m)
     pc = p.c()
     lib().oracle_forces_subset(C.byref(pc), n, _p(x, C.c_double), _p(v, C.c_double), _p(ids, C.c_uint32),
-                               int(step), float(eps), m, _p(sel, C.c_int64), _p(F, C.c_double),
+                               int(step), float(eps), float(eps_image), m, _p(sel, C.c_int64), _p(F, C.c_double),
                                _p(allow, C.c_double))
     return F, allow
 
@@ -278,8 +281,9 @@ def forces_celllist(p: DPDParams, x, v, step: int, ids=None):
     return F, int(npairs.value)
 
 
-def pairs(p: DPDParams, x, step: int, ids=None, eps: float = 0.0, cap: int | None = None):
+def pairs(p: DPDParams, x, step: int, ids=None, eps: float = 0.0, cap: int | None = None, eps_image=None):
     """Interacting or boundary pairs: returns (quad[k,4] = lo, hi, w0, w1; flag[k]) (T3)."""
+    eps_image = eps if eps_image is None else eps_image
     x = _f64(x)
     n = x.shape[0]
     ids = _ids(n, ids)
@@ -289,9 +293,9 @@ def pairs(p: DPDParams, x, step: int, ids=None, eps: float = 0.0, cap: int | Non
     quad = np.zeros((cap, 4), dtype=np.uint32)
     flag = np.zeros(cap, dtype=np.uint8)
     k = lib().oracle_pairs(C.byref(pc), n, _p(x, C.c_double), _p(ids, C.c_uint32), int(step),
-                           float(eps), cap, _p(quad, C.c_uint32), _p(flag, C.c_uint8))
+                           float(eps), float(eps_image), cap, _p(quad, C.c_uint32), _p(flag, C.c_uint8))
     if k > cap:
-        return pairs(p, x, step, ids, eps, cap=int(k))
+        return pairs(p, x, step, ids, eps, cap=int(k), eps_image=eps_image)
     return quad[:k].copy(), flag[:k].copy()
 
 

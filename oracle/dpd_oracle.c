@@ -262,13 +262,25 @@ static double boundary_bound(const oracle_params *p, double eps, const double vi
     return p->a * w + p->gamma * wR * wR * vabs + sigma * wR * fabs(xi) / sqrt(p->dt);
 }
 
+/* Boundary window of one pair (C-12): eps for pairs whose minimum image is the plain
+ * difference, eps_image for pairs that reach across a periodic edge (some d_k needed a
+ * shift by L_k): the fp32 path forms x_j + L_k there, which rounds at ulp(L_k). */
+static double pair_window(const oracle_params *p, const double xi[3], const double xj[3], double eps,
+                          double eps_image)
+{
+    for (int k = 0; k < 3; ++k)
+        if (rint((xi[k] - xj[k]) / p->box[k]) != 0.0) return eps_image;
+    return eps;
+}
+
 /* PairForces(x, v, s) -- the plain definition (C-1, C-2 item 4): for every particle i,
  * F_i = sum over all j != i of the pair force, minimum image, O(N^2).
  * x, v: n x 3 row-major; ids: global particle ids (C-7).
- * allow (may be NULL): per-particle sum of boundary_bound over pairs with |r - r_c| < eps
- *   (C-12); npairs (may be NULL): number of unordered interacting pairs. */
+ * allow (may be NULL): per-particle sum of boundary_bound over pairs with |r - r_c| below the
+ *   pair's window (eps, or eps_image across a periodic edge: pair_window, C-12);
+ *   npairs (may be NULL): number of unordered interacting pairs. */
 int oracle_forces(const oracle_params *p, int64_t n, const double *x, const double *v,
-                  const uint32_t *ids, int64_t step, double eps, double *F, double *allow,
+                  const uint32_t *ids, int64_t step, double eps, double eps_image, double *F, double *allow,
                   int64_t *npairs)
 {
     int64_t count = 0;
@@ -290,13 +302,14 @@ int oracle_forces(const oracle_params *p, int64_t n, const double *x, const doub
             }
             if (allow) {
                 double r = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-                if (fabs(r - p->rc) < eps) {
+                double w = pair_window(p, &x[3 * i], &x[3 * j], eps, eps_image);
+                if (fabs(r - p->rc) < w) {
                     if (!hit) {
                         uint32_t wds[2];
                         oracle_pair_words(p->seed, step, ids[i], ids[j], wds);
                         xi = oracle_xi(wds[0], wds[1]);
                     }
-                    al += boundary_bound(pp, eps, vij, xi);
+                    al += boundary_bound(pp, w, vij, xi);
                 }
             }
         }
@@ -313,8 +326,8 @@ int oracle_forces(const oracle_params *p, int64_t n, const double *x, const doub
  * oracle_forces for each selected i (sampled parity at full size, where the O(N^2) sweep
  * over every i is out of reach).  F and allow are m x 3 / m. */
 int oracle_forces_subset(const oracle_params *p, int64_t n, const double *x, const double *v,
-                         const uint32_t *ids, int64_t step, double eps, int64_t m, const int64_t *sel,
-                         double *F, double *allow)
+                         const uint32_t *ids, int64_t step, double eps, double eps_image, int64_t m,
+                         const int64_t *sel, double *F, double *allow)
 {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t k = 0; k < m; ++k) {
@@ -326,20 +339,22 @@ int oracle_forces_subset(const oracle_params *p, int64_t n, const double *x, con
             double d[3], vij[3], f[3], xi = 0.0;
             oracle_min_image(p, &x[3 * i], &x[3 * j], d);
             double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
-            if (r2 >= (p->rc + eps) * (p->rc + eps)) continue; /* no force, not a boundary pair */
+            double wmax = eps > eps_image ? eps : eps_image;
+            if (r2 >= (p->rc + wmax) * (p->rc + wmax)) continue; /* no force, not a boundary pair */
             for (int c = 0; c < 3; ++c) vij[c] = v[3 * i + c] - v[3 * j + c];
             oracle_params q;
             const oracle_params *pp = pair_params(p, i, j, &q);
             int hit = oracle_pair_force(pp, d, vij, ids[i], ids[j], step, f, &xi);
             if (hit) { Fi[0] += f[0]; Fi[1] += f[1]; Fi[2] += f[2]; }
             double r = sqrt(r2);
-            if (fabs(r - p->rc) < eps) {
+            double w = pair_window(p, &x[3 * i], &x[3 * j], eps, eps_image);
+            if (fabs(r - p->rc) < w) {
                 if (!hit) {
                     uint32_t wds[2];
                     oracle_pair_words(p->seed, step, ids[i], ids[j], wds);
                     xi = oracle_xi(wds[0], wds[1]);
                 }
-                al += boundary_bound(pp, eps, vij, xi);
+                al += boundary_bound(pp, w, vij, xi);
             }
         }
         F[3 * k + 0] = Fi[0];
@@ -351,12 +366,12 @@ int oracle_forces_subset(const oracle_params *p, int64_t n, const double *x, con
 }
 
 /* Enumerate unordered pairs (brute force), for pair-set / RNG-word parity (T3).
- * Every pair i<j that interacts (0 < r^2 < r_c^2) or lies within eps of the cutoff
- * (|r - r_c| < eps, a boundary pair, C-12) is written as (min id, max id, w0, w1) into
+ * Every pair i<j that interacts (0 < r^2 < r_c^2) or lies within its window of the cutoff
+ * (|r - r_c| < eps, or eps_image across a periodic edge: a boundary pair, C-12) is written as (min id, max id, w0, w1) into
  * quad[4*k..] with flag[k] = (interacts ? 1 : 0) | (boundary ? 2 : 0).  Returns the
  * total number of such pairs (may exceed cap; only the first cap are written). */
 int64_t oracle_pairs(const oracle_params *p, int64_t n, const double *x, const uint32_t *ids,
-                     int64_t step, double eps, int64_t cap, uint32_t *quad, uint8_t *flag)
+                     int64_t step, double eps, double eps_image, int64_t cap, uint32_t *quad, uint8_t *flag)
 {
     int64_t k = 0;
     for (int64_t i = 0; i < n; ++i) {
@@ -366,7 +381,7 @@ int64_t oracle_pairs(const oracle_params *p, int64_t n, const double *x, const u
             double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
             double r = sqrt(r2);
             int hit = (r2 > 0.0 && r2 < p->rc * p->rc);
-            int near = fabs(r - p->rc) < eps;
+            int near = fabs(r - p->rc) < pair_window(p, &x[3 * i], &x[3 * j], eps, eps_image);
             if (!hit && !near) continue;
             if (k < cap) {
                 uint32_t wds[2];
@@ -515,7 +530,7 @@ int64_t oracle_wall_carve(const oracle_params *p, int64_t n, const double *x, do
 int oracle_prime(const oracle_params *p, int64_t n, const double *x, const double *v,
                  const uint32_t *ids, int64_t step, double *F)
 {
-    return oracle_forces(p, n, x, v, ids, step, 0.0, F, NULL, NULL);
+    return oracle_forces(p, n, x, v, ids, step, 0.0, 0.0, F, NULL, NULL);
 }
 
 /* Groot-Warren velocity Verlet with lambda = 1/2, one force evaluation per step
@@ -535,7 +550,7 @@ int oracle_step(const oracle_params *p, int64_t n, double *x, double *v, double 
         memcpy(u, v, sizeof(double) * 3 * (size_t)n);
         oracle_kick_drift(p, n, x, u, F, 0.5 * p->dt);
         *step += 1;
-        oracle_forces(p, n, x, u, ids, *step, 0.0, F, NULL, NULL);
+        oracle_forces(p, n, x, u, ids, *step, 0.0, 0.0, F, NULL, NULL);
         for (int64_t i = 0; i < n; ++i) {
             if (is_frozen(p, i)) { /* the wall velocity, unchanged */
                 for (int k = 0; k < 3; ++k) v[3 * i + k] = u[3 * i + k];

@@ -137,3 +137,26 @@ def test_subset_sum_equals_full_sum():
     Fs, als = oracle.forces_subset(p, x, v, step=2, sel=sel, eps=1e-3)
     np.testing.assert_allclose(Fs, F[sel], rtol=0, atol=1e-12 * np.abs(F).max())
     np.testing.assert_allclose(als, allow[sel], rtol=1e-12, atol=1e-15)
+
+
+def test_boundary_window_per_pair():
+    # C-12: a pair within eps of r_c gets an allowance; a pair that reaches across a periodic
+    # edge uses the wider eps_image window (its fp32 image x_j + L rounds at ulp(L)).  A pair
+    # at r = r_c - 5e-6: inside the box it is a boundary pair only for eps > 5e-6; across
+    # the x edge it is one for eps_image > 5e-6 whatever eps is.
+    p = oracle.DPDParams(box=(8.0, 8.0, 8.0))
+    r = 1.0 - 5e-6
+    inside = np.array([[3.0, 4.0, 4.0], [3.0 + r, 4.0, 4.0]])
+    across = np.array([[0.2, 4.0, 4.0], [0.2 - r + 8.0, 4.0, 4.0]])
+    v = np.zeros((2, 3))
+    for x, img in [(inside, False), (across, True)]:
+        _, a_narrow, _ = oracle.forces(p, x, v, 0, eps=1e-6, eps_image=1e-6)
+        _, a_img, _ = oracle.forces(p, x, v, 0, eps=1e-6, eps_image=1e-5)
+        _, a_int, _ = oracle.forces(p, x, v, 0, eps=1e-5, eps_image=1e-6)
+        assert np.all(a_narrow == 0)
+        assert np.all(a_img > 0) == img and np.all(a_int > 0) == (not img)
+        # the subset sum and the pair enumeration use the same windows
+        _, s_img = oracle.forces_subset(p, x, v, 0, [0, 1], eps=1e-6, eps_image=1e-5)
+        np.testing.assert_array_equal(s_img, a_img)
+        _, flag = oracle.pairs(p, x, 0, eps=1e-6, eps_image=1e-5)
+        assert len(flag) == 1 and bool(flag[0] & 2) == img
