@@ -169,31 +169,81 @@ class ClockSampler:
 # CPU oracle leg (cpu_baseline and --impl reference): the oracle as it stands, fp64 cell-list
 # mode (C-2 item 7) on a bounded sub-box sample of the same workload (same rho / params).
 # ------------------------------------------------------------------------------------------
-def oracle_sample_rate(cfg, target_s=15.0, sample_box=24.0, max_steps=50):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_probe(cfg_name):
+    """The CPU legs of cpu_baseline, run in a child process with the
+    oracle built -O3 -march=native for this host (DPD_ORACLE_NATIVE=1; same source as the
+    parity build): brute force (the plain definition, C-1) on config 1 at 1 thread and at all
+    threads, and the fp64 cell-list mode (C-2 item 7) on the bench workload itself, full size,
+    all threads.  Each leg is bounded (a few seconds); prints one JSON object."""
     import oracle
-    box = tuple(min(float(b), sample_box) for b in cfg.box)
-    p = oracle.DPDParams(box=box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
-                         seed=cfg.seed, body_f=cfg.body_f)
-    pos, vel = workloads.make_particles(box, cfg.rho, cfg.kT)
-    st = oracle.State(p, pos, vel, celllist=True)
-    n = pos.shape[0]
-    t0 = time.perf_counter()
-    st.step(1)
-    dt1 = time.perf_counter() - t0
-    k = int(max(1, min(max_steps, target_s / max(dt1, 1e-6))))
-    t0 = time.perf_counter()
-    st.step(k)
-    el = time.perf_counter() - t0
-    return {"value": n * k / el, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"oracle fp64 cell-list mode, {k} steps of a {box[0]:g}x{box[1]:g}x{box[2]:g} sub-box "
-                      f"({n} particles) at the same rho={cfg.rho:g} and parameters as '{cfg.name}'"}
+    oracle.build(force=True)  # -march=native for the host this runs on
+    nthreads = oracle.num_threads()
+
+    def rate(cfg, celllist, budget_s, max_steps):
+        p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power,
+                             dt=cfg.dt, seed=cfg.seed, body_f=cfg.body_f)
+        pos, vel = workloads.make_config(cfg)
+        st = oracle.State(p, pos, vel, celllist=celllist)
+        n = pos.shape[0]
+        if not celllist:
+            st.step(2)  # thread-pool warm-up (the cell-list leg's step is seconds long)
+        t0 = time.perf_counter()
+        st.step(1)
+        dt1 = time.perf_counter() - t0
+        k = int(max(1, min(max_steps, budget_s / max(dt1, 1e-9))))
+        t0 = time.perf_counter()
+        st.step(k)
+        el = time.perf_counter() - t0
+        return {"value": n * k / el, "particles": n, "steps": k, "seconds": el}
+
+    c1 = workloads.CONFIGS["parity"]
+    cl = rate(workloads.CONFIGS[cfg_name], True, 12.0, 20)
+    bfn = rate(c1, False, 3.0, 400)
+    oracle.set_num_threads(1)
+    bf1 = rate(c1, False, 3.0, 200)
+    oracle.set_num_threads(nthreads)
+    print(json.dumps({"bf1": bf1, "bfn": bfn, "cl": cl, "threads": nthreads, "cpu_model": cpu_model(),
+                      "nproc": os.cpu_count(), "flags": " ".join(oracle.FLAGS)}), flush=True)
+
+
+def oracle_sample_rate(cfg):
+    """cpu_baseline: oracle_probe in a child process (its own -O3 -march=native oracle)."""
+    import subprocess
+    env = dict(os.environ, DPD_ORACLE_NATIVE="1")
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-probe", cfg.name], env=env,
+                       capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-400:])
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    cl, bf1, bfn = d["cl"], d["bf1"], d["bfn"]
+    return {"value": cl["value"], "unit": UNIT, "cores": d["threads"], "kind": "oracle",
+            "sample": f"oracle fp64 cell-list mode (C-2 item 7), {cl['steps']} steps of '{cfg.name}' itself "
+                      f"({cl['particles']} particles, full size), {d['threads']} threads",
+            "cpu_model": d["cpu_model"], "nproc": d["nproc"], "build": f"gcc {d['flags']} -fopenmp (same source "
+            "as the parity build, -O2)",
+            "brute_force_config1": {"workload": "parity: 8^3, rho=3, 1536 particles, O(N^2) all pairs (C-1)",
+                                    "threads_1": bf1["value"], f"threads_{d['threads']}": bfn["value"],
+                                    "unit": UNIT}}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    os.environ["DPD_ORACLE_NATIVE"] = "1"  # the same source, -O3 -march=native for this host
     import oracle
+    oracle.build(force=True)
     box = tuple(min(float(b), 24.0) for b in cfg.box)
     p = oracle.DPDParams(box=box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
                          seed=cfg.seed, body_f=cfg.body_f)
@@ -270,7 +320,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-kernel", type=int, default=None, help="0 tiled, 1 reference, 2 cell-warp")
     ap.add_argument("--option", action="append", default=[], help="engine option name=value (dpd_set_option)")
+    ap.add_argument("--oracle-probe", default=None, help=argparse.SUPPRESS)  # cpu_baseline child process
     args = ap.parse_args()
+    if args.oracle_probe:
+        oracle_probe(args.oracle_probe)
+        return 0
     args.warmup = max(args.warmup, 3)
     if args.config is None:
         args.config = "eq64" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "weak128"

@@ -169,7 +169,9 @@ int dpd_set_particles_ex(dpd_ctx *ctx, int64_t n, const float *pos, const float 
                          const int32_t *ids, int64_t step0);
 
 /* As dpd_set_particles_ex with a species index per particle (species may be NULL: all
- * 0).  An index outside [0, nspecies) is reported as DPD_ERR_ARG by this call. */
+ * 0).  An index outside [0, nspecies) is reported as DPD_ERR_ARG by this call, and so is a
+ * particle id >= 2^30 while a species matrix (nspecies > 1) is set: the tiled force kernel
+ * carries the species in the top two bits of the staged id word. */
 int dpd_set_particles_typed(dpd_ctx *ctx, int64_t n, const float *pos, const float *vel,
                             const int32_t *ids, const int32_t *species, int64_t step0);
 

@@ -18,17 +18,24 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dpd_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# DPD_ORACLE_NATIVE=1 (bench.py's CPU-timing legs only): the same source built -O3
+# -march=native for the host it runs on, as a separate library next to the parity build
+NATIVE = os.environ.get("DPD_ORACLE_NATIVE", "0") == "1"
+_LIB_NATIVE = os.path.join(_HERE, "liboracle_native.so")
+FLAGS = ["-O3", "-march=native"] if NATIVE else ["-O2"]
 
 
 def build(force: bool = False) -> str:
-    """Compile dpd_oracle.c with gcc (-O2, OpenMP).  Building the checker is not using it."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        cmd = ["gcc", "-O2", "-std=c11", "-D_DEFAULT_SOURCE", "-fopenmp", "-fPIC", "-shared",
+    """Compile dpd_oracle.c with gcc (-O2, OpenMP; -O3 -march=native under DPD_ORACLE_NATIVE=1).
+    Building the checker is not using it."""
+    out = _LIB_NATIVE if NATIVE else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        cmd = ["gcc", *FLAGS, "-std=c11", "-D_DEFAULT_SOURCE", "-fopenmp", "-fPIC", "-shared",
                "-Wall", "-Wextra", "-o", tmp, _SRC, "-lm"]
         subprocess.run(cmd, check=True)
-        os.replace(tmp, _LIB)
-    return _LIB
+        os.replace(tmp, out)
+    return out
 
 
 class Params(C.Structure):
@@ -138,6 +145,7 @@ def lib():
         L.oracle_step_celllist.argtypes = [P(Params), i64, dp, dp, dp, P(u32), P(i64), i64]
         L.oracle_step_celllist.restype = C.c_int
         L.oracle_num_threads.restype = C.c_int
+        L.oracle_set_num_threads.argtypes = [C.c_int]
         L.oracle_wall_sdf.argtypes = [P(Params), dp, dp]
         L.oracle_wall_sdf.restype = d
         L.oracle_kick_drift.argtypes = [P(Params), i64, dp, dp, dp, d]
@@ -164,6 +172,10 @@ def _ids(n, ids):
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    lib().oracle_set_num_threads(int(n))
 
 
 def philox4x32_10(ctr, key):
@@ -231,7 +243,7 @@ def min_image(p: DPDParams, xi_, xj_):
     return d
 
 
-def forces(p: DPDParams, x, v, step: int, ids=None, eps: float = 0.0, eps_image=None):
+def forces(p: DPDParams, x, v, step: int, ids=None, *, eps: float = 0.0, eps_image=None):
     """PairForces(x, v, s): O(N^2) minimum-image sum (C-1, C-2 item 4).
     Returns (F[n,3], allow[n], npairs); allow = boundary-pair allowance (C-12) over pairs
     within eps of r_c (eps_image, default eps, for pairs across a periodic edge)."""
@@ -249,7 +261,7 @@ def forces(p: DPDParams, x, v, step: int, ids=None, eps: float = 0.0, eps_image=
     return F, allow, int(npairs.value)
 
 
-def forces_subset(p: DPDParams, x, v, step: int, sel, ids=None, eps: float = 0.0, eps_image=None):
+def forces_subset(p: DPDParams, x, v, step: int, sel, ids=None, *, eps: float = 0.0, eps_image=None):
     """PairForces for the selected particles only (same all-j sum).  Returns (F[m,3], allow[m])."""
     eps_image = eps if eps_image is None else eps_image
     x, v = _f64(x), _f64(v)
@@ -281,7 +293,7 @@ def forces_celllist(p: DPDParams, x, v, step: int, ids=None):
     return F, int(npairs.value)
 
 
-def pairs(p: DPDParams, x, step: int, ids=None, eps: float = 0.0, cap: int | None = None, eps_image=None):
+def pairs(p: DPDParams, x, step: int, ids=None, *, eps: float = 0.0, cap: int | None = None, eps_image=None):
     """Interacting or boundary pairs: returns (quad[k,4] = lo, hi, w0, w1; flag[k]) (T3)."""
     eps_image = eps if eps_image is None else eps_image
     x = _f64(x)

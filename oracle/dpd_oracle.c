@@ -710,3 +710,13 @@ int oracle_num_threads(void)
     return 1;
 #endif
 }
+
+/* Thread count of the OpenMP loops (CPU-timing legs of bench.py: 1 thread and all). */
+void oracle_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}

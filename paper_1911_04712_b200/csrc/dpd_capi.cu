@@ -36,7 +36,6 @@
 
 #include "../../include/dpd.h"
 #include "dpd_dist.cuh"
-#include "dpd_force_cells.cuh"
 #include "dpd_force_tile.cuh"
 #include "dpd_kernels.cuh"
 #include "dpd_sched.h"
@@ -148,8 +147,7 @@ struct dpd_ctx {
     int wtype[DPD_MAX_WALLS] = {0};
     float wprm[DPD_MAX_WALLS][4] = {};
     float wvel[DPD_MAX_WALLS][3] = {};
-    int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel, 2: cell-warp
-    int tile_persistent = 0; // tiled kernel as resident CTAs walking the tiles (option "tile_persistent")
+    int force_impl = 0; // 0: tiled production kernel, 1: reference thread-per-particle kernel (cross-check)
     int nsm = 148;
     Geom geom{};
     PairP pp{};
@@ -203,6 +201,8 @@ struct dpd_ctx {
     std::string last_error;
     // NEXT-4: the step as a task graph and asynchronous dumps
     dpd::TaskGraph *step_graph[2] = {nullptr, nullptr}; // [0] plain step, [1] step + snapshot
+    dpd::TaskGraph *group_graph = nullptr;               // member 0 of an in-process group: its task-graph step
+    int group_graph_mode = 0; // member 0: dpd_group_step runs the production task graph (option "group_task_graph")
     IntegP ip_step{};
     cudaStream_t copy_stream = nullptr;
     DumpState *dump = nullptr;
@@ -321,6 +321,9 @@ int sync_check(dpd_ctx *c)
             return fail(c, DPD_ERR_CAPACITY, "device buffer capacity exceeded (particles, ghosts or migrants)");
         if (flags & ERR_SPECIES)
             return fail(c, DPD_ERR_ARG, "species index out of range (particle id %d; %d species)", id, c->nspecies);
+        if (flags & ERR_IDRANGE)
+            return fail(c, DPD_ERR_ARG, "particle id %d out of range: ids must be >= 0, and < 2^30 with a species "
+                        "matrix", id);
         if (flags & ERR_RANGE)
             return fail(c, DPD_ERR_NUMERIC,
                         "particle id %d moved more than one (sub)domain in a step or a pair force left the "
@@ -412,14 +415,16 @@ int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
     TRY(launch(c, KID_SCATTER, [&] {
         k_scatter<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p,
                                                               c->start[ss].p + g.ncell, g, ip, c->start[sd].p,
-                                                              c->rank_buf.p, c->pos[d].p, c->vel[d].p, c->frc[d].p);
+                                                              c->rank_buf.p, c->pos[d].p, c->vel[d].p, c->frc[d].p,
+                                                              (int)c->n_cap, c->err.p);
     }));
     if (with_mig) {
         const dim3 grid(nblk(c->mig.maxcap, 256), 27);
         const Msgs mr = c->mig.mr;
         TRY(launch(c, KID_MIGRATE, [&] {
             k_scatter_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->start[sd].p, c->rank_in.p,
-                                                        c->pos[d].p, c->vel[d].p, c->frc[d].p);
+                                                        c->pos[d].p, c->vel[d].p, c->frc[d].p, (int)c->n_cap,
+                                                        c->err.p);
         }));
     }
     c->cur = d;
@@ -479,34 +484,6 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const Geom g = c->geom;
     const PairP pp = c->pp;
-    if (c->force_impl == 2) {
-        const FixP fx = c->fix;
-        const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
-                          ((g.n[2] + FT_BZ - 1) / FT_BZ);
-        const size_t smem = sizeof(ForceCellSmem);
-        const int *st = c->start[c->scur].p;
-        return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
-#define DPD_CELLS(R, K)                                                                                             \
-    k_force_cells<R, K><<<ntile, FC_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, s_lo, \
-                                                             s_hi, rec, c->err.p)
-            if (record) {
-                switch (c->kmode) {
-                case 0: DPD_CELLS(true, 0); break;
-                case 1: DPD_CELLS(true, 1); break;
-                case 2: DPD_CELLS(true, 2); break;
-                default: DPD_CELLS(true, 3); break;
-                }
-            } else {
-                switch (c->kmode) {
-                case 0: DPD_CELLS(false, 0); break;
-                case 1: DPD_CELLS(false, 1); break;
-                case 2: DPD_CELLS(false, 2); break;
-                default: DPD_CELLS(false, 3); break;
-                }
-            }
-#undef DPD_CELLS
-        });
-    }
     if (c->force_impl == 0 || c->dist) {
         const FixP fx = c->fix;
         // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
@@ -514,20 +491,12 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         const PairP pp = scaled_pair(c->pp, fx.scale);
         const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp);
         const dim3 tgrid((g.n[0] + FT_BX - 1) / FT_BX, (g.n[1] + FT_BY - 1) / FT_BY, (g.n[2] + FT_BZ - 1) / FT_BZ);
-        const int ntile = ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) *
-                          ((g.n[2] + FT_BZ - 1) / FT_BZ);
         const size_t smem = sizeof(ForceTileSmem);
         const int *st = c->start[c->scur].p;
         return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
 #define DPD_TILE(R, K)                                                                                              \
-    do {                                                                                                            \
-        if (c->tile_persistent)                                                                                     \
-            k_force_tile_p<R, K><<<std::min(ntile, c->nsm * 3), FT_NTHR, smem, c->stream>>>(                        \
-                c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, c->err.p);                               \
-        else                                                                                                        \
-            k_force_tile<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp,   \
-                                                                    fx, rk, rec, c->err.p);                         \
-    } while (0)
+    k_force_tile<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, \
+                                                            c->err.p)
             if (record) {
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;
@@ -613,7 +582,7 @@ int phase_halo_force(dpd_ctx *c, int64_t step)
     k_force_halo_cells<K><<<nbh, 32 * kHcWarps, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, c->blist.p,  \
                                                                 c->start[c->scur].p, c->gpos.p, c->gvel.p,          \
                                                                 c->gstart.p, g, pp, c->fix.scale, c->fix.inv_scale, \
-                                                                s_lo, s_hi)
+                                                                c->fix.mag_lim, s_lo, s_hi, c->err.p)
         switch (c->kmode) {
         case 0: DPD_HALO(0); break;
         case 1: DPD_HALO(1); break;
@@ -656,16 +625,19 @@ int exchange_nccl(dpd_ctx *c, MsgArea &m, cudaStream_t st)
 #endif
 }
 
-int exchange_group(dpd_ctx **g, int n, bool ghosts)
+// st: the stream of the copy (default: the group's shared compute stream); padded: copy the
+// capacity-padded slots, the volume the NCCL transport sends (the group's task-graph step).
+int exchange_group(dpd_ctx **g, int n, bool ghosts, cudaStream_t st = nullptr, bool padded = false)
 {
-    // one k_group_copy launch per kCopyJobs messages (all members share one stream)
+    // one k_group_copy launch per kCopyJobs messages
     CopyJobs jobs;
     int nj = 0;
+    if (!st) st = g[0]->stream;
     auto flush = [&]() -> int {
         if (nj == 0) return DPD_OK;
         dpd_ctx *c = g[0];
         TRY(launch(c, ghosts ? KID_GHOST_PACK : KID_MIGRATE,
-                   [&] { k_group_copy<<<dim3(16, nj), 256, 0, c->stream>>>(jobs); }));
+                   [&] { k_group_copy<<<dim3(padded ? 64 : 16, nj), 256, 0, st>>>(jobs); }, st));
         nj = 0;
         return DPD_OK;
     };
@@ -680,6 +652,7 @@ int exchange_group(dpd_ctx **g, int n, bool ghosts)
             jobs.j[nj].src = reinterpret_cast<const int4 *>(m.send.p + m.ms.off[d]);
             jobs.j[nj].dst = reinterpret_cast<int4 *>(pm.recv.p + pm.mr.off[d]);
             jobs.j[nj].cap = m.ms.cap[d];
+            jobs.j[nj].full = padded ? 1 : 0;
             if (++nj == kCopyJobs) TRY(flush());
         }
     }
@@ -994,8 +967,91 @@ int group_prime(dpd_ctx **g, int n)
     return DPD_OK;
 }
 
+// The in-process group's step as one task graph: the production step of build_step_graph for
+// every member -- kick_drift_bin -> migrate_exchange -> scan_scatter -> [ghost_pack ->
+// ghost_exchange -> ghost_sort] on the member's communication stream, concurrent with
+// force_local on the compute stream -> halo_force -- with the NCCL send/recv tasks swapped
+// for one device copy of every member's capacity-padded messages (the bytes NCCL sends).
+// Slot 0 = the group's compute stream, slot 1 + r = member r's communication stream;
+// cross-slot edges are CUDA events (TaskGraph::run).
+dpd::TaskGraph *build_group_graph(dpd_ctx **g, int n)
+{
+    auto *G = new dpd::TaskGraph();
+    std::vector<int> bin(n), sort(n), pack(n), gsort(n), force(n);
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        bin[r] = G->add("kick_drift_bin", 0, [c](cudaStream_t) {
+            const float kick = c->primed ? (float)(0.5 * c->dt) : (float)c->dt;
+            c->ip_step = integ(c, (float)c->dt, kick);
+            return phase_bin(c, c->ip_step);
+        });
+    }
+    const int mx = G->add("migrate_exchange", 0, [g, n](cudaStream_t s) { return exchange_group(g, n, false, s, true); });
+    for (int r = 0; r < n; ++r) G->edge(bin[r], mx);
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        sort[r] = G->add("scan_scatter", 0, [c](cudaStream_t) -> int {
+            TRY(phase_sort(c, c->ip_step));
+            c->step += 1;
+            return DPD_OK;
+        });
+        G->edge(mx, sort[r]);
+    }
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        pack[r] = G->add("ghost_pack", 1 + r, [c](cudaStream_t s) { return phase_ghost_pack(c, s); });
+        G->edge(sort[r], pack[r]);
+    }
+    const int gx = G->add("ghost_exchange", 1, [g, n](cudaStream_t s) { return exchange_group(g, n, true, s, true); });
+    for (int r = 0; r < n; ++r) G->edge(pack[r], gx);
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        gsort[r] = G->add("ghost_sort", 1 + r, [c](cudaStream_t s) { return phase_ghost_sort(c, s); });
+        G->edge(gx, gsort[r]);
+    }
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        force[r] = G->add("force_local", 0, [c](cudaStream_t) {
+            return force_pass(c, c->step, c->frc[c->cur].p, PairRec{nullptr, nullptr, 0}, false);
+        });
+        G->edge(sort[r], force[r]);
+    }
+    for (int r = 0; r < n; ++r) {
+        dpd_ctx *c = g[r];
+        const int h = G->add("halo_force", 0, [c](cudaStream_t) {
+            const int rc = phase_halo_force(c, c->step);
+            c->primed = false;
+            return rc;
+        });
+        G->edge(force[r], h);
+        G->edge(gsort[r], h);
+    }
+    if (G->build() != 0) {
+        delete G;
+        return nullptr;
+    }
+    return G;
+}
+
+int group_step_graph(dpd_ctx **g, int n)
+{
+    dpd_ctx *c0 = g[0];
+    if (!c0->group_graph) {
+        c0->group_graph = build_group_graph(g, n);
+        if (!c0->group_graph) return fail(c0, DPD_ERR_CONFIG, "group task graph has a cycle");
+    }
+    std::vector<cudaStream_t> streams(1 + n);
+    streams[0] = c0->stream;
+    for (int r = 0; r < n; ++r) streams[1 + r] = g[r]->comm_stream ? g[r]->comm_stream : c0->stream;
+    const int rc = c0->group_graph->run(streams.data());
+    if (rc == -1) return fail(c0, DPD_ERR_CONFIG, "group task graph has a cycle");
+    if (rc == -2) return fail(c0, DPD_ERR_CUDA, "group task graph: %s", cudaGetErrorString(cudaGetLastError()));
+    return rc;
+}
+
 int group_step(dpd_ctx **g, int n)
 {
+    if (g[0]->group_graph_mode) return group_step_graph(g, n);
     IntegP ip[64];
     for (int r = 0; r < n; ++r) {
         dpd_ctx *c = g[r];
@@ -1109,33 +1165,18 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
     pp.seed_hi = (uint32_t)(seed >> 32);
     c->pp = pp;
     set_fixed_scale(c, a, gamma);
-    c->fix.prune = 1;
     {
-        // two tiles per SM need the maximum shared-memory carveout (2 x (smem + 1 KB) <= 228 KB)
+        // three tiles per SM need the maximum shared-memory carveout (3 x (smem + 1 KB) <= 228 KB)
         const int smem = (int)sizeof(ForceTileSmem);
-        const void *fns[16] = {(const void *)k_force_tile<false, 0>,   (const void *)k_force_tile<false, 1>,
-                               (const void *)k_force_tile<false, 2>,   (const void *)k_force_tile<false, 3>,
-                               (const void *)k_force_tile<true, 0>,    (const void *)k_force_tile<true, 1>,
-                               (const void *)k_force_tile<true, 2>,    (const void *)k_force_tile<true, 3>,
-                               (const void *)k_force_tile_p<false, 0>, (const void *)k_force_tile_p<false, 1>,
-                               (const void *)k_force_tile_p<false, 2>, (const void *)k_force_tile_p<false, 3>,
-                               (const void *)k_force_tile_p<true, 0>,  (const void *)k_force_tile_p<true, 1>,
-                               (const void *)k_force_tile_p<true, 2>,  (const void *)k_force_tile_p<true, 3>};
+        const void *fns[8] = {(const void *)k_force_tile<false, 0>, (const void *)k_force_tile<false, 1>,
+                              (const void *)k_force_tile<false, 2>, (const void *)k_force_tile<false, 3>,
+                              (const void *)k_force_tile<true, 0>,  (const void *)k_force_tile<true, 1>,
+                              (const void *)k_force_tile<true, 2>,  (const void *)k_force_tile<true, 3>};
         int dev = 0;
         CUDA_TRY(c, cudaGetDevice(&dev));
         CUDA_TRY(c, cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
         for (const void *f : fns) {
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                             (int)cudaSharedmemCarveoutMaxShared));
-        }
-        const int smc = (int)sizeof(ForceCellSmem);
-        const void *fcs[8] = {(const void *)k_force_cells<false, 0>, (const void *)k_force_cells<false, 1>,
-                              (const void *)k_force_cells<false, 2>, (const void *)k_force_cells<false, 3>,
-                              (const void *)k_force_cells<true, 0>,  (const void *)k_force_cells<true, 1>,
-                              (const void *)k_force_cells<true, 2>,  (const void *)k_force_cells<true, 3>};
-        for (const void *f : fcs) {
-            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smc));
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxShared));
         }
@@ -1250,6 +1291,7 @@ void dpd_destroy(dpd_ctx *c)
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     if (c->dump) dpd_dump_close(c, nullptr);
     for (auto *g : c->step_graph) delete g;
+    delete c->group_graph;
     for (int b = 0; b < 2; ++b) {
         c->pos[b].release();
         c->vel[b].release();
@@ -1323,25 +1365,20 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
 {
     if (!c || !name) return DPD_ERR_ARG;
     if (strcmp(name, "force_kernel") == 0) {
-        if (value < 0 || value > 2)
-            return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled), 1 (reference) or 2 (cell-warp)");
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled) or 1 (reference)");
         if (value != 0 && c->dist) return fail(c, DPD_ERR_ARG, "force_kernel %d is single-domain only", (int)value);
         c->force_impl = (int)value;
         return DPD_OK;
     }
-    if (strcmp(name, "tile_persistent") == 0) {
-        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "tile_persistent must be 0 or 1");
-        c->tile_persistent = (int)value;
+    if (strcmp(name, "group_task_graph") == 0) {
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "group_task_graph must be 0 or 1");
+        if (!c->group || c->group[0] != c) return fail(c, DPD_ERR_ARG, "group_task_graph is set on member 0 of a group");
+        c->group_graph_mode = (int)value;
         return DPD_OK;
     }
     if (strcmp(name, "body_force_mode") == 0) {
         if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "body_force_mode must be 0 or 1");
         c->body_mode = (int)value;
-        return DPD_OK;
-    }
-    if (strcmp(name, "row_pruning") == 0) {
-        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "row_pruning must be 0 or 1");
-        c->fix.prune = (int)value;
         return DPD_OK;
     }
     if (strcmp(name, "dump_delay_us") == 0) {

@@ -20,13 +20,15 @@ __global__ void k_zero_headers(Msgs m)
 
 // In-process group transport: every (sender, direction) message of one exchange in one
 // launch (blockIdx.y = job).  Copies the int4 count header and the min(count, cap) particles
-// actually packed (two int4 each), not the capacity-padded slot; an overflowing count is
-// copied as is so the receiver raises ERR_CAPACITY (msg_received).
+// actually packed (two int4 each) -- or, with full set, the whole capacity-padded slot, the
+// bytes the NCCL transport sends; an overflowing count is copied as is so the receiver
+// raises ERR_CAPACITY (msg_received).
 constexpr int kCopyJobs = 512;
 struct CopyJob {
     const int4 *src;
     int4 *dst;
     int cap;
+    int full;
 };
 struct CopyJobs {
     CopyJob j[kCopyJobs];
@@ -35,7 +37,7 @@ struct CopyJobs {
 __global__ void __launch_bounds__(256) k_group_copy(const __grid_constant__ CopyJobs jobs)
 {
     const CopyJob &J = jobs.j[blockIdx.y];
-    const int cnt = min(max(J.src[0].x, 0), J.cap);
+    const int cnt = J.full ? J.cap : min(max(J.src[0].x, 0), J.cap);
     const int total = 1 + 2 * cnt;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) J.dst[k] = J.src[k];
 }
@@ -50,20 +52,24 @@ __device__ __forceinline__ int msg_received(const Msgs &m, int d, int *err)
     return c;
 }
 
-// Cell coordinate of a received ghost along one dimension: halo layers map to -1 / n in
-// split dimensions (x in [-h, 0) / [L, L + h)), interior otherwise (C-8 formula).
-__device__ __forceinline__ int ghost_coord(float x, float inv_h, int n, int split)
+// Cell coordinate of a received ghost along one dimension: in split dimensions a ghost
+// below 0 / at or above L lies in the halo layer -1 / n (decided by the sign test, not by
+// floor(x n / L), whose fp32 product can round L + tiny into interior cell n - 1); interior
+// positions use the C-8 formula.
+__device__ __forceinline__ int ghost_coord(float x, float inv_h, int n, int split, float L)
 {
-    if (!split) return cell_coord(x, inv_h, n);
-    const int q = (int)floorf(__fmul_rn(x, inv_h));
-    return min(max(q, -1), n);
+    if (split) {
+        if (x < 0.0f) return -1;
+        if (x >= L) return n;
+    }
+    return cell_coord(x, inv_h, n);
 }
 
 __device__ __forceinline__ int ghost_cell(const Geom &g, float x, float y, float z)
 {
-    const int ix = ghost_coord(x, g.inv_h[0], g.n[0], g.split[0]) + g.off[0];
-    const int iy = ghost_coord(y, g.inv_h[1], g.n[1], g.split[1]) + g.off[1];
-    const int iz = ghost_coord(z, g.inv_h[2], g.n[2], g.split[2]) + g.off[2];
+    const int ix = ghost_coord(x, g.inv_h[0], g.n[0], g.split[0], g.L[0]) + g.off[0];
+    const int iy = ghost_coord(y, g.inv_h[1], g.n[1], g.split[1], g.L[1]) + g.off[1];
+    const int iz = ghost_coord(z, g.inv_h[2], g.n[2], g.split[2], g.L[2]) + g.off[2];
     return ix + g.ext[0] * (iy + g.ext[1] * iz);
 }
 
@@ -89,7 +95,8 @@ __global__ void __launch_bounds__(256) k_bin_recv(Msgs rec, Geom g, int maxcap, 
 
 __global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxcap, const int *__restrict__ start,
                                                       const int *__restrict__ rank_in, float4 *__restrict__ pos_o,
-                                                      float4 *__restrict__ vel_o, float4 *__restrict__ frc_o)
+                                                      float4 *__restrict__ vel_o, float4 *__restrict__ frc_o, int cap,
+                                                      int *err)
 {
     const int d = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -100,6 +107,10 @@ __global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxc
     if (r < 0) return;
     const float4 p = msg_data(rec, d)[2 * k], v = msg_data(rec, d)[2 * k + 1];
     const int dst = start[cell_index(g, p.x, p.y, p.z)] + r;
+    if (dst >= cap) { // more particles than the member's arrays hold: DPD_ERR_CAPACITY
+        raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
+        return;
+    }
     pos_o[dst] = p;
     vel_o[dst] = v;
     frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                        const int *__restrict__ bcells, const int *__restrict__ start,
                        const float4 *__restrict__ gpos, const float4 *__restrict__ gvel,
                        const int *__restrict__ gstart, Geom g, PairP pp, float scale, float inv_scale,
-                       uint32_t s_lo, uint32_t s_hi)
+                       float mag_lim, uint32_t s_lo, uint32_t s_hi, int *err)
 {
     __shared__ unsigned qbuf[kHcWarps][32 + 32 * kHcI]; // < 32 pending + kHcI x 32 new
     __shared__ float4 spi[kHcWarps][32];                // the cell's local positions (broadcast reads)
@@ -282,6 +293,7 @@ __global__ void __launch_bounds__(32 * kHcWarps)
     unsigned *q = qbuf[warp];
     const uint32_t ks = step_key(s_lo, s_hi, pp.seed_lo, pp.seed_hi);
     const int nbc = bcells[0];
+    float amax = 0.0f; // largest pair force magnitude: the fixed-point range check
     for (int w = blockIdx.x * kHcWarps + warp; w < nbc; w += gridDim.x * kHcWarps) {
         const int gc = bcells[1 + w];
         const int ci[3] = {gc % g.ext[0] - g.off[0], (gc / g.ext[0]) % g.ext[1] - g.off[1],
@@ -332,8 +344,11 @@ __global__ void __launch_bounds__(32 * kHcWarps)
                     const float rx = ix - (pj.x + shx), ry = iy - (pj.y + shy), rz = iz - (pj.z + shz);
                     const float r2 = rx * rx + ry * ry + rz * rz;
                     const float dv = rx * (ux - vj.x) + ry * (uy - vj.y) + rz * (uz - vj.z);
-                    const float sc = pair_scalar<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(iw),
-                                                        (uint32_t)__float_as_int(pj.w), ks, uw, vj.w);
+                    float mag;
+                    const float sc = pair_mag<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(iw),
+                                                     (uint32_t)__float_as_int(pj.w), ks, __float_as_int(uw),
+                                                     __float_as_int(vj.w), mag);
+                    amax = fmaxf(amax, fabsf(mag));
                     atomicAdd(&acc[warp][0][ii], __float_as_int(__fmaf_rn(sc * rx, scale, 12582912.0f)) - 0x4B400000);
                     atomicAdd(&acc[warp][1][ii], __float_as_int(__fmaf_rn(sc * ry, scale, 12582912.0f)) - 0x4B400000);
                     atomicAdd(&acc[warp][2][ii], __float_as_int(__fmaf_rn(sc * rz, scale, 12582912.0f)) - 0x4B400000);
@@ -404,6 +419,7 @@ __global__ void __launch_bounds__(32 * kHcWarps)
             __syncwarp();
         }
     }
+    if (amax > mag_lim) raise_err(err, ERR_RANGE, 0); // |f scale| >= 2^21: DPD_ERR_NUMERIC
 }
 
 } // namespace dpd

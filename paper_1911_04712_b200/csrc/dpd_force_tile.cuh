@@ -1,8 +1,8 @@
 // dpd_force_tile.cuh -- production pair-force sweep for sm_100a.
 //
 // One CTA of 9 warps per tile of BX x BY x BZ home cells (cell lists, symmetric
-// forces), 3 tiles resident per SM (74 KB shared memory, 72 registers); launched on a 3D grid,
-// one CTA per tile (or, option tile_persistent, as resident CTAs walking the tiles):
+// forces), 3 tiles resident per SM (73 KB shared memory, 72 registers); launched on a 3D grid,
+// one CTA per tile:
 //   1. table   : one warp loads the staged cell table of the forward half-stencil region,
 //                (BX+2) x (BY+2) x (BZ+1) cells, straight from the cell starts and scans it;
 //                another warp scans the home rows;
@@ -58,7 +58,6 @@ struct FixP {
     float inv_scale; // 2^-k
     float mag_lim;   // 2^21 / scale: larger pair magnitudes raise ERR_RANGE
     float slack;     // row-end pruning: distance bounds are lowered by this much
-    int prune;       // row-end pruning on (1, default) / off (0): engine option "row_pruning"
 };
 
 // Cell table of one tile (SURVEY §8a row a5 staging): staged cell -> smem / global start,
@@ -78,8 +77,7 @@ struct ForceTileSmem {
     int acc[3][FT_SCAP];                         // fixed-point force sums
     int4 wrec[FT_NWARP * FT_WSTRIDE];            // per warp, compacted owners: {list prefix, prefix + count,
                                                  //   list base minus prefix, staged index} (one LDS.128)
-    TileTab tab[2];                              // cell tables: current tile / next tile (persistent)
-    int done_cnt;                                // persistent kernel: warps done with their pairs
+    TileTab tab[1];                              // the tile's cell table
     int nown;                                    // owners with a non-empty list
 };
 
@@ -497,29 +495,11 @@ __device__ void tile_fallback(const float4 *__restrict__ pos, const float4 *__re
 }
 
 // ---------------------------------------------------------------------------------------
-// Tile phases (shared by the one-tile-per-CTA kernel and the persistent kernel).
+// Tile phases.
 // ---------------------------------------------------------------------------------------
 struct TileGeo {
     int x0, y0, z0, bx, by, bz;
 };
-
-__device__ __forceinline__ TileGeo tile_geo(int t, const Geom &g)
-{
-    const int ntx = (g.n[0] + FT_BX - 1) / FT_BX, nty = (g.n[1] + FT_BY - 1) / FT_BY;
-    TileGeo G;
-    G.x0 = (t % ntx) * FT_BX;
-    G.y0 = ((t / ntx) % nty) * FT_BY;
-    G.z0 = (t / (ntx * nty)) * FT_BZ;
-    G.bx = min(FT_BX, g.n[0] - G.x0);
-    G.by = min(FT_BY, g.n[1] - G.y0);
-    G.bz = min(FT_BZ, g.n[2] - G.z0);
-    return G;
-}
-
-__device__ __forceinline__ int tile_count(const Geom &g)
-{
-    return ((g.n[0] + FT_BX - 1) / FT_BX) * ((g.n[1] + FT_BY - 1) / FT_BY) * ((g.n[2] + FT_BZ - 1) / FT_BZ);
-}
 
 // 1a. staged cell table straight from global memory.  role 0 (one warp): one staged row per
 // lane -- its cells' starts and counts, a warp scan of the row sums, the in-row prefix;
@@ -684,7 +664,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
                 int a = (k == 0) ? s_i + 1 : T.soff[cs];
                 int b = T.soff[cs + (k == 0 ? 2 : 3)];
-                if (k > 0 && fx.prune) {
+                if (k > 0) {
                     const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
                     const float qz = (k == 1) ? 0.0f : dzr;
                     const float q = qy * qy + qz * qz;
@@ -848,72 +828,6 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     tile_pairs<RECORD, KMODE>(S, T, G, g, pp, fx, ks, rec, err, tid, warp, lane);
     __syncthreads();
     tile_flush(S, T, G, g, fx, frc, warp, lane);
-}
-
-// Persistent variant: gridDim.x resident CTAs walk the tiles t = blockIdx.x + k gridDim.x.
-// While tile t's pairs finish, the first two warps done load tile t + gridDim.x's cell table
-// into the second buffer; its staging copies are issued before tile t's flush (the staging
-// area and the lists are free by then), so their latency overlaps the flush.
-template <bool RECORD, int KMODE>
-__global__ void __launch_bounds__(FT_NTHR, FT_MINB)
-    k_force_tile_p(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
-                   const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
-                   PairRec rec, int *err)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const RoundKeys &ks = rk;
-    const int ntile = tile_count(g);
-    int t = blockIdx.x, b = 0;
-    if (t >= ntile) return;
-    TileGeo G = tile_geo(t, g);
-    if (warp < 2) tile_table(S.tab[0], G, g, start, warp, lane);
-    if (tid == 0) S.done_cnt = 0;
-    __syncthreads();
-    bool fb = tile_overflows(S.tab[0], G);
-    if (!fb) {
-        tile_stage_issue(S, S.tab[0], G, g, pos, vel, warp, lane);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
-        tile_stage_fix<KMODE>(S, S.tab[0], G, g, warp, lane);
-    }
-    __syncthreads();
-    for (;;) {
-        const int tn = t + gridDim.x;
-        const bool more = tn < ntile;
-        const TileGeo Gn = more ? tile_geo(tn, g) : G;
-        if (fb) {
-            if (tid == 0) atomicAdd(&err[S.tab[b].total > FT_SCAP ? 4 : 5], 1);
-            tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, G.x0, G.y0, G.z0, G.bx, G.by,
-                                         G.bz, fx.inv_scale);
-        } else {
-            tile_pairs<RECORD, KMODE>(S, S.tab[b], G, g, pp, fx, ks, rec, err, tid, warp, lane);
-        }
-        if (more) {
-            int order = 0;
-            if (lane == 0) order = atomicAdd(&S.done_cnt, 1);
-            order = __shfl_sync(0xffffffffu, order, 0);
-            if (order < 2) tile_table(S.tab[b ^ 1], Gn, g, start, order, lane);
-        }
-        __syncthreads(); // pairs of t done, next table ready
-        const bool fbn = more && tile_overflows(S.tab[b ^ 1], Gn);
-        if (more && !fbn) tile_stage_issue(S, S.tab[b ^ 1], Gn, g, pos, vel, warp, lane);
-        if (!fb) tile_flush(S, S.tab[b], G, g, fx, frc, warp, lane);
-        if (tid == 0) S.done_cnt = 0;
-        __syncthreads(); // the sums of t are flushed
-        if (!more) break;
-        if (!fbn) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-            tile_stage_fix<KMODE>(S, S.tab[b ^ 1], Gn, g, warp, lane);
-        }
-        __syncthreads();
-        t = tn;
-        G = Gn;
-        b ^= 1;
-        fb = fbn;
-    }
 }
 
 } // namespace dpd

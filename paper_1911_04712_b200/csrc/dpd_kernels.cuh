@@ -14,7 +14,7 @@
 namespace dpd {
 
 // Error word bits (device int err[4]: [0] flags, [1] offending id, [2] overflow amount)
-enum : int { ERR_NONFINITE = 1, ERR_CAPACITY = 2, ERR_RANGE = 4, ERR_SPECIES = 8 };
+enum : int { ERR_NONFINITE = 1, ERR_CAPACITY = 2, ERR_RANGE = 4, ERR_SPECIES = 8, ERR_IDRANGE = 16 };
 
 __device__ __forceinline__ void raise_err(int *err, int bit, int id)
 {
@@ -207,6 +207,8 @@ __global__ void k_pack_input(const float *__restrict__ pos3, const float *__rest
             raise_err(err, ERR_SPECIES, id);
             sp = 0;
         }
+        // the tiled force kernel carries the species in bits 30-31 of the staged id word
+        if (id < 0 || (nspecies > 1 && id >= (1 << 30))) raise_err(err, ERR_IDRANGE, id);
         p4 = make_float4(x, y, z, __int_as_float(id));
         v4 = make_float4(vx, vy, vz, __int_as_float(sp)); // w: species index (NEXT-2)
     }
@@ -448,7 +450,8 @@ __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos,
                                                  const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
                                                  IntegP ip, const int *__restrict__ start,
                                                  const int *__restrict__ rank, float4 *__restrict__ pos_o,
-                                                 float4 *__restrict__ vel_o, float4 *__restrict__ frc_o)
+                                                 float4 *__restrict__ vel_o, float4 *__restrict__ frc_o, int cap,
+                                                 int *err)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= *n_ptr || rank[i] < 0) return; // rank < 0: migrant, sent away
@@ -459,6 +462,10 @@ __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos,
         xn = make_float3(0.0f, 0.0f, 0.0f);
     const int c = cell_index(g, xn.x, xn.y, xn.z);
     const int dst = start[c] + rank[i];
+    if (dst >= cap) { // a decomposed member gained more particles than its arrays hold
+        raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
+        return;
+    }
     pos_o[dst] = make_float4(xn.x, xn.y, xn.z, p.w);
     vel_o[dst] = make_float4(un.x, un.y, un.z, v.w); // w: species
     frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);

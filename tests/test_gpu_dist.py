@@ -32,16 +32,13 @@ def destroy(capi, ctxs):
         capi.dpd_destroy(c)
 
 
-@pytest.mark.parametrize("persistent", [0, 1])
 @pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 1), (2, 2, 2), (3, 1, 2)])
-def test_group_prime_forces_match_oracle(grid, persistent):
+def test_group_prime_forces_match_oracle(grid):
     cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
     p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
                          seed=cfg.seed)
     pos0, vel0 = workloads.make_config(cfg)
     capi, ctxs = make_group(cfg, grid)
-    for c in ctxs:  # the tiled kernel with halo rings, one CTA per tile or resident CTAs
-        capi.dpd_set_option(c, "tile_persistent", persistent)
     try:
         ids0 = np.arange(pos0.shape[0], dtype=np.int32)
         for c in ctxs:  # every member receives the global set and keeps its own share
@@ -59,10 +56,15 @@ def test_group_prime_forces_match_oracle(grid, persistent):
         destroy(capi, ctxs)
 
 
+@pytest.mark.parametrize("graph", [0, 1])
 @pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 2)])
-def test_group_per_step_parity_with_migration(grid):
+def test_group_per_step_parity_with_migration(grid, graph):
     """30 steps at dt = 0.01 (config-1 parameters): particles migrate between subdomains; each
-    step the oracle recomputes F(x_s, u_s, s) from the gathered GPU state (C-13)."""
+    step the oracle recomputes F(x_s, u_s, s) from the gathered GPU state (C-13).  graph = 1
+    runs the production step: the task graph of build_step_graph for every member (ghost
+    pack / exchange / sort on the communication streams, concurrent with the interior forces,
+    CUDA-event edges) with the NCCL send/recv swapped for a device copy of the same
+    capacity-padded messages."""
     cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
     p = oracle.DPDParams(box=cfg.box, rc=cfg.rc, a=cfg.a, gamma=cfg.gamma, kT=cfg.kT, power=cfg.power, dt=cfg.dt,
                          seed=cfg.seed)
@@ -70,6 +72,7 @@ def test_group_per_step_parity_with_migration(grid):
     n = pos0.shape[0]
     capi, ctxs = make_group(cfg, grid)
     try:
+        capi.dpd_set_option(ctxs[0], "group_task_graph", graph)
         ids0 = np.arange(n, dtype=np.int32)
         for c in ctxs:
             capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
@@ -89,7 +92,8 @@ def test_group_per_step_parity_with_migration(grid):
         destroy(capi, ctxs)
 
 
-def test_group_matches_single_domain():
+@pytest.mark.parametrize("graph", [0, 1])
+def test_group_matches_single_domain(graph):
     """Same initial state on one domain and on a 2x2x2 group: forces after 5 steps agree to
     fp32 accuracy (identical RNG words: global ids key the pair RNG, C-7/C-19)."""
     from paper_1911_04712_b200 import capi
@@ -99,6 +103,7 @@ def test_group_matches_single_domain():
     single.set_particles(pos0, vel0)
     _, ctxs = make_group(cfg, (2, 2, 2))
     try:
+        capi.dpd_set_option(ctxs[0], "group_task_graph", graph)
         ids0 = np.arange(pos0.shape[0], dtype=np.int32)
         for c in ctxs:
             capi.dpd_set_particles_ex(c, pos0, vel0, ids0, 0)
@@ -224,5 +229,36 @@ def test_group_empty_and_one_sided_sets():
         assert sum(counts) == pos1.shape[0] and min(counts[1:]) > 0
         ids = np.concatenate([gather_state(capi, [c])[3] for c in ctxs])
         assert np.array_equal(np.sort(ids), ids1)
+    finally:
+        destroy(capi, ctxs)
+
+
+@pytest.mark.parametrize("graph", [0, 1])
+def test_member_array_capacity_overflow_is_reported(graph):
+    """A dense block drifting into an empty member fills that member's particle arrays (sized
+    at set time from its own share: 1.1 n + 12 sqrt(n) + 4096) past their capacity: the step
+    reports DPD_ERR_CAPACITY (the scatter refuses slots beyond the arrays) instead of writing
+    past them."""
+    from paper_1911_04712_b200 import capi
+    # force-free particles (a = gamma = kT = 0): the slab drifts intact at u = 3 along x
+    cfg = workloads.Config("capacity", (12.0, 12.0, 12.0), 3.0, 0.0, 0.0, 0.0, 0.5, 0.01)
+    rng = np.random.default_rng(3)
+    n = 9000
+    pos = np.empty((n, 3), np.float32)
+    pos[:, 0] = 4.9 + rng.random(n) * 1.0  # a slab against member 1's face at x = 6
+    pos[:, 1:] = rng.random((n, 2)) * 12.0
+    vel = np.zeros((n, 3), np.float32)
+    vel[:, 0] = 3.0
+    _, ctxs = make_group(cfg, (2, 1, 1))
+    try:
+        capi.dpd_set_option(ctxs[0], "group_task_graph", graph)
+        ids = np.arange(n, dtype=np.int32)
+        for c in ctxs:
+            capi.dpd_set_option(c, "message_capacity_percent", 100000)  # the messages are not the limit
+            capi.dpd_set_particles_ex(c, pos, vel, ids, 0)
+        assert capi.dpd_get_count(ctxs[1]) == 0
+        with pytest.raises(capi.DPDError) as e:
+            capi.dpd_group_step(ctxs, 60)
+        assert e.value.code == capi.DPD_ERR_CAPACITY
     finally:
         destroy(capi, ctxs)

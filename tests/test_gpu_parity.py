@@ -16,15 +16,12 @@ pytestmark = pytest.mark.gpu
 FORCE_TOL = 1e-4
 
 
-KERNELS = [0, 1, 2, "0p"]  # 0: tiled, 1: reference, 2: cell-warp, 0p: tiled as a persistent kernel
+KERNELS = [0, 1]  # 0: tiled (production), 1: reference thread-per-particle (cross-check)
 
 
 def _ctx(cfg, seed=None, kernel=0):
     from paper_1911_04712_b200 import capi
     d = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed if seed is None else seed)
-    if kernel == "0p":
-        d.set_option("tile_persistent", 1)
-        kernel = 0
     d.set_option("force_kernel", kernel)
     return d
 
@@ -36,7 +33,35 @@ def _params(cfg):
 
 def boundary_eps(box):
     # fp32 positions near L carry an absolute error of ~ulp(L); widen the C-12 window to it
+    # (used where the GPU works in shifted local frames: the decomposed group tests)
     return max(1e-5, 16 * float(np.spacing(np.float32(max(box)))))
+
+
+def windows(box, rc=1.0):
+    """Per-pair C-12 windows (eps, eps_image): a pair inside the box differs from the fp64
+    definition only by the fp32 rounding of r^2 (a few ulp of r_c); a pair across a
+    periodic edge also carries the rounding of the shifted image x_j +- L (<= ulp(L) / 2
+    per coordinate, sqrt(3)/2 ulp(L) in r)."""
+    eps = 4.0 * float(np.spacing(np.float32(rc)))
+    return eps, max(eps, 2.0 * float(np.spacing(np.float32(max(box)))))
+
+
+def window_kw(box, rc=1.0):
+    eps, eps_img = windows(box, rc)
+    return {"eps": eps, "eps_image": eps_img}
+
+
+def face_sample(pos, box, n_random, n_face, seed):
+    """Particle indices: n_random uniform ones plus n_face within r_c of each of the six
+    periodic faces (the pairs that cross a periodic edge)."""
+    rng = np.random.default_rng(seed)
+    n = pos.shape[0]
+    sel = [rng.choice(n, n_random, replace=False)]
+    for d in range(3):
+        for near in (pos[:, d] < 1.0, pos[:, d] >= box[d] - 1.0):
+            idx = np.flatnonzero(near)
+            sel.append(rng.choice(idx, min(n_face, idx.size), replace=False))
+    return np.unique(np.concatenate(sel))
 
 
 def by_id(ids, *arrays):
@@ -143,15 +168,22 @@ def test_errors_are_reported():
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_per_step_parity_config1(kernel):
-    """100 steps of config 1 (C-13): each step, the oracle is fed the GPU state."""
+@pytest.mark.parametrize("body_f", [0.0, 2.0])
+def test_per_step_parity_config1(kernel, body_f):
+    """100 steps of config 1 (C-13): each step, the oracle is fed the GPU state.  Forces,
+    cells, pair words, and the integrator against oracle.kick_drift (C-6), with and
+    without the periodic-Poiseuille body force."""
     cfg = workloads.CONFIGS["parity"]
     p = _params(cfg)
-    eps = boundary_eps(cfg.box)
+    p.body_f = body_f
+    eps, eps_img = windows(cfg.box)
     pos0, vel0 = workloads.make_config(cfg)
     d = _ctx(cfg, kernel=kernel)
+    if body_f:
+        d.set_body_force(body_f)
     d.set_particles(pos0, vel0)
     n = pos0.shape[0]
+    box = np.array(cfg.box)
     prev = None
     worst = 0.0
     kick = 0.5 * cfg.dt
@@ -167,22 +199,22 @@ def test_per_step_parity_config1(kernel):
         assert np.array_equal(cell, ocell)
         # storage order is cell-sorted: cells of consecutive slots are non-decreasing
         assert np.all(np.diff(ocell[ids]) >= 0)
-        # forces F_s = F(x_s, u_s, s)
-        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps)
+        # forces F_s = F(x_s, u_s, s), per-pair boundary windows (C-12)
+        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps, eps_image=eps_img)
         worst = max(worst, check_forces(F_id, F_ref, allow))
-        # integrator: x_{s} = wrap(x_{s-1} + dt (u_{s-1} + kick F_{s-1})), u_s = u_{s-1} + kick F_{s-1}
+        # integrator: the oracle's kick-drift of the previous GPU state (kick dt/2 after set,
+        # dt after: the fused second + first half kicks, C-6)
         if prev is not None:
             px, pu, pF, pk = prev
-            u_pred = pu.astype(np.float64) + pk * pF.astype(np.float64)
-            x_pred = px.astype(np.float64) + cfg.dt * u_pred
+            x_pred, u_pred, _ = oracle.kick_drift(p, px, pu, pF, pk)
             dx = x_id - x_pred
-            dx -= np.array(cfg.box) * np.rint(dx / np.array(cfg.box))
+            dx -= box * np.rint(dx / box)
             assert np.abs(dx).max() < 2e-6
             assert np.abs(u_id - u_pred).max() < 1e-5 * (1 + np.abs(u_pred).max())
         # pair set and RNG words, every 20 steps (T3)
         if s % 20 == 0:
             quad = d.debug_pairs()
-            oq, oflag = oracle.pairs(p, x_id, s, eps=eps)
+            oq, oflag = oracle.pairs(p, x_id, s, eps=eps, eps_image=eps_img)
             gset = {tuple(r) for r in quad.tolist()}
             core = {tuple(r) for r, f in zip(oq.tolist(), oflag) if (f & 1) and not (f & 2)}
             boundary = {tuple(r) for r, f in zip(oq.tolist(), oflag) if f & 2}
@@ -194,6 +226,73 @@ def test_per_step_parity_config1(kernel):
         if s < cfg.steps:
             d.step(1)
     print(f"worst relative force error {worst:.2e}")
+
+
+@pytest.mark.parametrize("body_f", [0.0, 2.0])
+def test_full_step_velocity_matches_oracle(body_f):
+    """Row a6: dpd_get_particles returns the full-step velocity v = u + dt/2 (F + f_body)
+    (C-6).  From one initial state, one and three GPU steps against oracle.State's
+    GW-VV steps, element by element (fp32 vs fp64; a few steps are far from chaotic
+    divergence, C-13)."""
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    p.body_f = body_f
+    eps, eps_img = windows(cfg.box)
+    pos0, vel0 = workloads.make_config(cfg)
+    box = np.array(cfg.box)
+    for k in (1, 3):
+        d = _ctx(cfg)
+        if body_f:
+            d.set_body_force(body_f)
+        d.set_particles(pos0, vel0)
+        d.step(k)
+        x, v = d.get_particles()
+        st = oracle.State(p, pos0, vel0).step(k)
+        dx = x - st.x
+        dx -= box * np.rint(dx / box)
+        assert np.abs(dx).max() < 1e-5 * k
+        _, allow, _ = oracle.forces(p, st.x, st.u, k, eps=eps, eps_image=eps_img)
+        tol = cfg.dt * k * (FORCE_TOL * np.abs(st.F).max() + allow[:, None]) + 1e-5 * (1 + np.abs(st.v))
+        err = np.abs(v.astype(np.float64) - st.v)
+        assert np.all(err <= tol), (k, err.max(), tol.min())
+        # and the velocity really is the full-step one: the half-step u differs by dt/2 F
+        assert np.abs(st.v - st.u).max() > 10 * tol.max()
+
+
+def test_edge_pairs_coincident_cutoff_and_range():
+    """Degenerate pairs of the method (P:121-122 strict cutoff, S:191-192 r = 0): coincident
+    particles exert no force; a pair at exactly r = r_c does not interact; a pair whose force
+    leaves the fixed-point range reports DPD_ERR_NUMERIC instead of a wrong sum."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    d = _ctx(cfg)
+    v = np.array([[0.3, -0.2, 0.1], [-0.1, 0.4, 0.0], [0.2, 0.1, -0.3]], np.float32)
+    # r = 0: particles 0 and 1 coincide; particle 2 at r = 0.5 from both
+    x = np.array([[2.0, 3.0, 4.0], [2.0, 3.0, 4.0], [2.5, 3.0, 4.0]], np.float32)
+    d.set_particles(x, v)
+    F = d.get_forces()
+    F_ref, _, npairs = oracle.forces(p, x, v, 0)
+    assert npairs == 2 and np.all(np.isfinite(F))
+    check_forces(F, F_ref, np.zeros(3))
+    # r = r_c exactly (1.0 in fp32 and fp64): no pair, zero force; and across the periodic x edge
+    for x in (np.array([[2.0, 3.0, 4.0], [3.0, 3.0, 4.0]], np.float32),
+              np.array([[0.5, 3.0, 4.0], [7.5, 3.0, 4.0]], np.float32)):
+        d.set_particles(x, v[:2])
+        assert np.all(d.get_forces() == 0.0)
+        assert d.debug_pairs().shape[0] == 0
+    # just inside r_c interacts
+    d.set_particles(np.array([[2.0, 3.0, 4.0], [2.9999, 3.0, 4.0]], np.float32), v[:2])
+    assert np.abs(d.get_forces()).max() > 0
+    # fixed-point range: a relative speed of 1e4 at r = 0.5 gives |F^D| ~ 1e5, far beyond the
+    # scale's bound (a + 6.7 sigma / sqrt(dt) + 20 gamma): reported, never silently wrapped
+    fast = np.array([[2.0, 3.0, 4.0], [2.5, 3.0, 4.0]], np.float32)
+    with pytest.raises(capi.DPDError) as e:
+        d.set_particles(fast, np.array([[1e4, 0, 0], [-1e4, 0, 0]], np.float32))
+    assert e.value.code == capi.DPD_ERR_NUMERIC
+    # the context stays usable after the error
+    d.set_particles(fast, v[:2])
+    assert np.all(np.isfinite(d.get_forces()))
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
@@ -209,7 +308,28 @@ def test_dense_cluster_overflow_fallback(kernel):
     vel = rng.normal(size=pos.shape).astype(np.float32)
     d = _ctx(cfg, kernel=kernel)
     d.set_particles(pos, vel)
-    F_ref, allow, _ = oracle.forces(p, pos, vel, 0, eps=boundary_eps(cfg.box))
+    F_ref, allow, _ = oracle.forces(p, pos, vel, 0, **window_kw(cfg.box))
+    check_forces(d.get_forces(), F_ref, allow)
+
+
+def test_crowded_cell_full_list_path():
+    """One cell holding 40 particles inside a tile that still fits shared memory: the first
+    particles of that cell find more partners than a list holds (FT_LCAP), so the tiled
+    kernel evaluates the rest in place (stat "full_list_particles"); forces must still be
+    the oracle's."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    rng = np.random.default_rng(11)
+    crowd = (rng.random((40, 3)) * 0.9 + np.array([3.05, 4.05, 2.05])).astype(np.float32)
+    fluid = (rng.random((1500, 3)) * 8.0).astype(np.float32)
+    pos = np.concatenate([crowd, fluid])
+    vel = rng.normal(size=pos.shape).astype(np.float32)
+    d = _ctx(cfg, kernel=0)
+    d.set_particles(pos, vel)
+    assert capi.dpd_get_stat(d.ctx, "full_list_particles") > 0
+    assert capi.dpd_get_stat(d.ctx, "fallback_tiles") == 0
+    F_ref, allow, _ = oracle.forces(p, pos, vel, 0, **window_kw(cfg.box))
     check_forces(d.get_forces(), F_ref, allow)
 
 
@@ -313,7 +433,7 @@ def test_full_size_sampled_parity(name, kernel):
     particles against the oracle's all-j sums, plus size-independent properties."""
     cfg = workloads.CONFIGS[name]
     p = _params(cfg)
-    eps = boundary_eps(cfg.box)
+    eps, eps_img = windows(cfg.box)
     pos0, vel0 = workloads.make_config(cfg)
     d = _ctx(cfg, kernel=kernel)
     d.set_particles(pos0, vel0)
@@ -321,9 +441,11 @@ def test_full_size_sampled_parity(name, kernel):
     pos, u, F, ids = d.get_state()
     n = pos.shape[0]
     assert np.array_equal(np.sort(ids), np.arange(n))
-    rng = np.random.default_rng(0)
-    sel = rng.choice(n, 64, replace=False)
-    F_ref, allow = oracle.forces_subset(p, pos, u, d.get_step(), sel, ids=ids.astype(np.uint32), eps=eps)
+    # >= 4096 particles: 2048 uniform + 384 within r_c of each periodic face
+    sel = face_sample(pos, cfg.box, 2048, 384, seed=0)
+    assert sel.size >= 4096
+    F_ref, allow = oracle.forces_subset(p, pos, u, d.get_step(), sel, ids=ids.astype(np.uint32), eps=eps,
+                                        eps_image=eps_img)
     scale = np.abs(F).max()
     err = np.abs(F[sel].astype(np.float64) - F_ref).max(axis=1)
     assert np.all(err <= FORCE_TOL * scale + allow), (err.max(), scale)
@@ -348,7 +470,7 @@ def test_per_step_parity_ragged_boxes(box, rho, kernel):
     forces within the bar, every particle accounted for."""
     cfg = workloads.Config("ragged", box, rho, 25.0, 4.5, 1.0, 0.5, 0.01)
     p = _params(cfg)
-    eps = boundary_eps(cfg.box)
+    eps, eps_img = windows(cfg.box)
     pos0, vel0 = workloads.make_config(cfg)
     d = _ctx(cfg, kernel=kernel)
     d.set_particles(pos0, vel0)
@@ -360,7 +482,7 @@ def test_per_step_parity_ragged_boxes(box, rho, kernel):
         cell, count, start = d.debug_cells()
         ocell, ocount, ostart = oracle.cells(p, x_id)
         assert np.array_equal(count, ocount) and np.array_equal(start, ostart) and np.array_equal(cell, ocell)
-        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps)
+        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps, eps_image=eps_img)
         check_forces(F_id, F_ref, allow)
         if s < 10:
             d.step(1)
@@ -373,7 +495,7 @@ def test_full_size_sampled_parity_other_configs(name):
     oracle, cell counts bit-exact, sum F = 0."""
     cfg = workloads.CONFIGS[name]
     p = _params(cfg)
-    eps = boundary_eps(cfg.box)
+    eps, eps_img = windows(cfg.box)
     pos0, vel0 = workloads.make_config(cfg)
     d = _ctx(cfg)
     if cfg.body_f:
@@ -383,9 +505,11 @@ def test_full_size_sampled_parity_other_configs(name):
     pos, u, F, ids = d.get_state()
     n = pos.shape[0]
     assert n == pos0.shape[0]
-    rng = np.random.default_rng(1)
-    sel = rng.choice(n, 32, replace=False)
-    F_ref, allow = oracle.forces_subset(p, pos, u, d.get_step(), sel, ids=ids.astype(np.uint32), eps=eps)
+    # >= 1024 particles: 512 uniform + 96 within r_c of each periodic face
+    sel = face_sample(pos, cfg.box, 512, 96, seed=1)
+    assert sel.size >= 1024
+    F_ref, allow = oracle.forces_subset(p, pos, u, d.get_step(), sel, ids=ids.astype(np.uint32), eps=eps,
+                                        eps_image=eps_img)
     scale = np.abs(F).max()
     err = np.abs(F[sel].astype(np.float64) - F_ref).max(axis=1)
     assert np.all(err <= FORCE_TOL * scale + allow), (err.max(), scale)
