@@ -292,6 +292,30 @@ def rank_particles(cfg, world, rank, scaling="weak"):
     return pos, vel, ids, coord, sub
 
 
+def weak_point(capi, stream, torch, steps, warmup):
+    """BASELINE config 4 (128^3, rho = 8) on this one GPU: particle-steps/s over `steps`
+    device-timed steps after `warmup`, inputs resident."""
+    cfg = workloads.CONFIGS["weak128"]
+    ctx = capi.dpd_create(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
+    try:
+        capi.dpd_set_stream(ctx, stream.cuda_stream)
+        pos, vel = workloads.make_config(cfg)
+        capi.dpd_set_particles_ex(ctx, pos, vel, None, 0)
+        capi.dpd_step(ctx, warmup)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        capi.dpd_step_async(ctx, steps)
+        e1.record(stream)
+        capi.dpd_sync(ctx)
+        ms = e0.elapsed_time(e1)
+        return {"value": cfg.n * steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+                "workload": "weak128: 128^3 rho=8 (16,777,216 particles), BASELINE config 4 on one GPU -- the "
+                            "per-GPU workload of the N > 1 weak-scaling lines"}
+    finally:
+        capi.dpd_destroy(ctx)
+
+
 def config_block(cfg, args, world):
     g = rank_grid(world)
     strong = getattr(args, "scaling", "weak") == "strong"
@@ -318,6 +342,7 @@ def main():
                          "(BASELINE config 5: --config strong256 --scaling strong)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-weak-point", action="store_true", help="skip the 128^3 N = 1 weak-series point")
     ap.add_argument("--force-kernel", type=int, default=None, help="0 tiled, 1 reference, 2 cell-warp")
     ap.add_argument("--option", action="append", default=[], help="engine option name=value (dpd_set_option)")
     ap.add_argument("--oracle-probe", default=None, help=argparse.SUPPRESS)  # cpu_baseline child process
@@ -471,6 +496,12 @@ def main():
                              "frac": step_bytes_gbs / hbm, "peak_source": peaks_src},
            "kernels": per_kernel, "kernel_ms_per_step": step_kernel_ms, "e2e": e2e,
            "force_fallback_tiles": capi.dpd_get_stat(ctx, "fallback_tiles")}
+
+    # --- the weak series' N = 1 point: the driver's scaling run times this same command at N =
+    # 1 (BASELINE config 2, 64^3) and N > 1 (config 4, one 128^3 subdomain per GPU); the
+    # config-4 workload on this one GPU, same timing rules, is recorded beside it
+    if world == 1 and args.config == "eq64" and not args.no_weak_point:
+        out["weak128_n1"] = weak_point(capi, stream, torch, max(5, min(args.steps, 20)), args.warmup)
 
     if rank == 0 and not args.no_cpu_baseline:
         try:
