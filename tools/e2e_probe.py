@@ -21,7 +21,7 @@ for rep in range(3):
     capi.dpd_set_particles_ex(ctx, pos_h, vel_h, None, 0)
     t1 = time.perf_counter()
     ev[1].record(stream)
-    capi.dpd_step_async(ctx, 200)
+    capi.dpd_step_async(ctx, int(os.environ.get("K", "200")))
     ev[2].record(stream)
     capi.dpd_get_particles(ctx, out_pos, out_vel)
     ev[3].record(stream)
