@@ -116,8 +116,11 @@ struct RoundKeys {
 __device__ __forceinline__ uint2 pair_words(uint32_t ida, uint32_t idb, const RoundKeys &K)
 {
     uint32_t c0 = min(ida, idb), c1 = max(ida, idb);
+#ifndef PROBE_ROUNDS
+#define PROBE_ROUNDS 10
+#endif
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < PROBE_ROUNDS; ++r) {
         const uint32_t hi = __umulhi(kPhilox2M, c0), lo = kPhilox2M * c0;
         c0 = hi ^ K.k[r] ^ c1;
         c1 = lo;

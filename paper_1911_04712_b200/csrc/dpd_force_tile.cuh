@@ -260,7 +260,8 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src)
                  : "memory");
 }
 
-__device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__restrict__ pos,
+template <class SM>
+__device__ __forceinline__ void stage_copy(SM &S, const float4 *__restrict__ pos,
                                            const float4 *__restrict__ vel, int g0, int s0, int len, int lane)
 {
     for (int k = lane; k < len; k += 32) {
@@ -271,8 +272,8 @@ __device__ __forceinline__ void stage_copy(ForceTileSmem &S, const float4 *__res
 
 // Second pass over a staged range: periodic-image shift, SoA copy, id (| species << 30) into
 // the velocity word, zeroed accumulators.
-template <int KMODE>
-__device__ __forceinline__ void stage_fix(ForceTileSmem &S, int s0, int len, float sx, float sy, float sz, int lane)
+template <int KMODE, class SM>
+__device__ __forceinline__ void stage_fix(SM &S, int s0, int len, float sx, float sy, float sz, int lane)
 {
     for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
@@ -427,9 +428,15 @@ __device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &
     c.fx += qx;
     c.fy += qy;
     c.fz += qz;
+#if defined(PROBE_JATOM) && PROBE_JATOM == 1
+    (void)j; { const int jj = threadIdx.x; atomicAdd(&S.acc[0][jj], -qx); atomicAdd(&S.acc[1][jj], -qy); atomicAdd(&S.acc[2][jj], -qz); }
+#elif defined(PROBE_JATOM) && PROBE_JATOM == 2
+    (void)j; if ((qx ^ qy ^ qz) == 0x7fffffff) S.acc[0][0] = 1;
+#else
     atomicAdd(&S.acc[0][j], -qx); // native ATOMS.ADD (the fp32 variant is a CAS loop)
     atomicAdd(&S.acc[1][j], -qy);
     atomicAdd(&S.acc[2][j], -qz);
+#endif
     ++c.t;
 }
 
@@ -571,7 +578,8 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
 }
 
 // 1b. issue the staging copies of this warp's rows (cp.async, not waited for).
-__device__ __forceinline__ void tile_stage_issue(ForceTileSmem &S, const TileTab &T, const TileGeo &G,
+template <class SM>
+__device__ __forceinline__ void tile_stage_issue(SM &S, const TileTab &T, const TileGeo &G,
                                                  const Geom &g, const float4 *__restrict__ pos,
                                                  const float4 *__restrict__ vel, int warp, int lane)
 {
@@ -591,8 +599,8 @@ __device__ __forceinline__ void tile_stage_issue(ForceTileSmem &S, const TileTab
 }
 
 // 1b (second half, after cp.async.wait_all): periodic shift, SoA copy, ids, zeroed sums.
-template <int KMODE>
-__device__ __forceinline__ void tile_stage_fix(ForceTileSmem &S, const TileTab &T, const TileGeo &G, const Geom &g,
+template <int KMODE, class SM>
+__device__ __forceinline__ void tile_stage_fix(SM &S, const TileTab &T, const TileGeo &G, const Geom &g,
                                                int warp, int lane)
 {
     const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
@@ -658,8 +666,11 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             const float dzr = fmaxf(hz - oz - fx.slack, 0.0f);
             unsigned lptr = lbase;
             bool full = false;
+#ifndef PROBE_NOSWEEP
+#define PROBE_NOSWEEP 0
+#endif
 #pragma unroll // all five segments (measured 457 -> 449 us against a rolled loop)
-            for (int k = 0; k < 5; ++k) {
+            for (int k = 0; k < (PROBE_NOSWEEP ? 0 : 5); ++k) {
                 // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
                 const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
                 int a = (k == 0) ? s_i + 1 : T.soff[cs];
@@ -720,7 +731,10 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
         // ---- 4. pair evaluation: contiguous chunk of the warp's lists per lane, walked by two
         //         independent cursors (halves of the chunk) so two Philox/Box-Muller chains
         //         are in flight per thread (instruction-level parallelism)
-        if (tot > 0) {
+#ifndef PROBE_NOPAIR
+#define PROBE_NOPAIR 0
+#endif
+        if (tot > 0 && !PROBE_NOPAIR) {
             const int C = (tot + 31) >> 5;
             const int t0 = min(lane * C, tot);
             const int t1 = min(t0 + C, tot);
@@ -764,7 +778,8 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 
 // 5. flush: fixed point -> fp32, one vector reduction per staged particle; rows map back
 // to <= 3 contiguous global segments, exactly as they were staged.
-__device__ __forceinline__ void tile_flush(const ForceTileSmem &S, const TileTab &T, const TileGeo &G,
+template <class SM>
+__device__ __forceinline__ void tile_flush(const SM &S, const TileTab &T, const TileGeo &G,
                                            const Geom &g, const FixP &fx, float4 *frc, int warp, int lane)
 {
     const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
