@@ -36,7 +36,6 @@
 
 #include "../../include/dpd.h"
 #include "dpd_dist.cuh"
-#include "dpd_force_cb.cuh"
 #include "dpd_force_tile.cuh"
 #include "dpd_kernels.cuh"
 #include "dpd_sched.h"
@@ -485,35 +484,6 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const Geom g = c->geom;
     const PairP pp = c->pp;
-    if (c->force_impl == 2) {
-        const FixP fx = c->fix;
-        const PairP pp = scaled_pair(c->pp, fx.scale);
-        const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp);
-        const dim3 tgrid((g.n[0] + FT_BX - 1) / FT_BX, (g.n[1] + FT_BY - 1) / FT_BY, (g.n[2] + FT_BZ - 1) / FT_BZ);
-        const size_t smem = sizeof(ForceCBSmem);
-        const int *st = c->start[c->scur].p;
-        return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
-#define DPD_CB(R, K)                                                                                                \
-    k_force_cb<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, \
-                                                          c->err.p)
-            if (record) {
-                switch (c->kmode) {
-                case 0: DPD_CB(true, 0); break;
-                case 1: DPD_CB(true, 1); break;
-                case 2: DPD_CB(true, 2); break;
-                default: DPD_CB(true, 3); break;
-                }
-            } else {
-                switch (c->kmode) {
-                case 0: DPD_CB(false, 0); break;
-                case 1: DPD_CB(false, 1); break;
-                case 2: DPD_CB(false, 2); break;
-                default: DPD_CB(false, 3); break;
-                }
-            }
-#undef DPD_CB
-        });
-    }
     if (c->force_impl == 0 || c->dist) {
         const FixP fx = c->fix;
         // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
@@ -1210,16 +1180,6 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
             CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                              (int)cudaSharedmemCarveoutMaxShared));
         }
-        const int smem_cb = (int)sizeof(ForceCBSmem);
-        const void *fcb[8] = {(const void *)k_force_cb<false, 0>, (const void *)k_force_cb<false, 1>,
-                              (const void *)k_force_cb<false, 2>, (const void *)k_force_cb<false, 3>,
-                              (const void *)k_force_cb<true, 0>,  (const void *)k_force_cb<true, 1>,
-                              (const void *)k_force_cb<true, 2>,  (const void *)k_force_cb<true, 3>};
-        for (const void *f : fcb) {
-            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cb));
-            CUDA_TRY(c, cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                             (int)cudaSharedmemCarveoutMaxShared));
-        }
     }
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
@@ -1405,9 +1365,8 @@ int dpd_set_option(dpd_ctx *c, const char *name, int64_t value)
 {
     if (!c || !name) return DPD_ERR_ARG;
     if (strcmp(name, "force_kernel") == 0) {
-        if (value < 0 || value > 2)
-            return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled), 1 (reference) or 2 (cell-block)");
-        if (value == 1 && c->dist) return fail(c, DPD_ERR_ARG, "force_kernel %d is single-domain only", (int)value);
+        if (value < 0 || value > 1) return fail(c, DPD_ERR_ARG, "force_kernel must be 0 (tiled) or 1 (reference)");
+        if (value != 0 && c->dist) return fail(c, DPD_ERR_ARG, "force_kernel %d is single-domain only", (int)value);
         c->force_impl = (int)value;
         return DPD_OK;
     }

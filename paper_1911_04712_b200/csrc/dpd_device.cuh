@@ -116,7 +116,7 @@ struct RoundKeys {
 __device__ __forceinline__ uint2 pair_words(uint32_t ida, uint32_t idb, const RoundKeys &K)
 {
     uint32_t c0 = min(ida, idb), c1 = max(ida, idb);
-#ifndef PROBE_ROUNDS
+#ifndef PROBE_ROUNDS // timing probe only (tools/build_variants.sh): other values break C-7 parity
 #define PROBE_ROUNDS 10
 #endif
 #pragma unroll

@@ -428,15 +428,9 @@ __device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &
     c.fx += qx;
     c.fy += qy;
     c.fz += qz;
-#if defined(PROBE_JATOM) && PROBE_JATOM == 1
-    (void)j; { const int jj = threadIdx.x; atomicAdd(&S.acc[0][jj], -qx); atomicAdd(&S.acc[1][jj], -qy); atomicAdd(&S.acc[2][jj], -qz); }
-#elif defined(PROBE_JATOM) && PROBE_JATOM == 2
-    (void)j; if ((qx ^ qy ^ qz) == 0x7fffffff) S.acc[0][0] = 1;
-#else
     atomicAdd(&S.acc[0][j], -qx); // native ATOMS.ADD (the fp32 variant is a CAS loop)
     atomicAdd(&S.acc[1][j], -qy);
     atomicAdd(&S.acc[2][j], -qz);
-#endif
     ++c.t;
 }
 
@@ -666,7 +660,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             const float dzr = fmaxf(hz - oz - fx.slack, 0.0f);
             unsigned lptr = lbase;
             bool full = false;
-#ifndef PROBE_NOSWEEP
+#ifndef PROBE_NOSWEEP // timing probes: compile the sweep / pair walk out; wrong forces
 #define PROBE_NOSWEEP 0
 #endif
 #pragma unroll // all five segments (measured 457 -> 449 us against a rolled loop)

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 FORCE_TOL = 1e-4
 
 
-KERNELS = [0, 1, 2]  # 0: tiled, 1: reference thread-per-particle (cross-check), 2: cell-block
+KERNELS = [0, 1]  # 0: tiled (production), 1: reference thread-per-particle (cross-check)
 
 
 def _ctx(cfg, seed=None, kernel=0):

@@ -23,7 +23,7 @@ def _params(cfg, sp):
                             dt=cfg.dt, seed=cfg.seed, amat=A3, gmat=G3, species=sp)
 
 
-@pytest.mark.parametrize("kernel", [0, 1, 2])
+@pytest.mark.parametrize("kernel", [0, 1])
 @pytest.mark.parametrize("power", [0.5, 1.0])
 def test_prime_forces_match_oracle(kernel, power):
     from paper_1911_04712_b200 import capi
