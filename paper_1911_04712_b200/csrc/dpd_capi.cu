@@ -394,11 +394,15 @@ int phase_bin(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
 }
 
 // a10 (received side) + a3 + a4: histogram of the migrants, scan, scatter; flips cur/scur.
-int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
+// The target force buffer frc[d] must be zero: inside a step the previous force pass zeroed
+// it (k_force_tile's fzero); a re-sort outside a step (set, carve) passes zero_target.
+int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true, bool zero_target = false)
 {
     const Geom g = c->geom;
     const int s = c->cur, d = 1 - c->cur;
     const int ss = c->scur, sd = 1 - c->scur;
+    if (zero_target && c->n_cap > 0)
+        CUDA_TRY(c, cudaMemsetAsync(c->frc[d].p, 0, sizeof(float4) * (size_t)c->n_cap, c->stream));
     with_mig = with_mig && c->dist;
     if (with_mig) {
         const dim3 grid(nblk(c->mig.maxcap, 256), 27);
@@ -415,16 +419,15 @@ int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
     TRY(launch(c, KID_SCATTER, [&] {
         k_scatter<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p,
                                                               c->start[ss].p + g.ncell, g, ip, c->start[sd].p,
-                                                              c->rank_buf.p, c->pos[d].p, c->vel[d].p, c->frc[d].p,
-                                                              (int)c->n_cap, c->err.p);
+                                                              c->rank_buf.p, c->pos[d].p, c->vel[d].p, (int)c->n_cap,
+                                                              c->err.p);
     }));
     if (with_mig) {
         const dim3 grid(nblk(c->mig.maxcap, 256), 27);
         const Msgs mr = c->mig.mr;
         TRY(launch(c, KID_MIGRATE, [&] {
             k_scatter_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->start[sd].p, c->rank_in.p,
-                                                        c->pos[d].p, c->vel[d].p, c->frc[d].p, (int)c->n_cap,
-                                                        c->err.p);
+                                                        c->pos[d].p, c->vel[d].p, (int)c->n_cap, c->err.p);
         }));
     }
     c->cur = d;
@@ -484,6 +487,9 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const Geom g = c->geom;
     const PairP pp = c->pp;
+    // the step's force pass also zeroes the other force buffer (the next sort's target)
+    float4 *fzero = (frc_out == c->frc[b].p) ? c->frc[1 - b].p : nullptr;
+    const int nzero = fzero ? (int)c->n_cap : 0;
     if (c->force_impl == 0 || c->dist) {
         const FixP fx = c->fix;
         // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
@@ -496,7 +502,7 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
 #define DPD_TILE(R, K)                                                                                              \
     k_force_tile<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, \
-                                                            c->err.p)
+                                                            c->err.p, fzero, nzero)
             if (record) {
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;
@@ -515,6 +521,7 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
 #undef DPD_TILE
         });
     }
+    if (fzero && nzero > 0) CUDA_TRY(c, cudaMemsetAsync(fzero, 0, sizeof(float4) * (size_t)nzero, c->stream));
     const int n = (int)c->n;
     if (n == 0) return DPD_OK;
     const int *st = c->start[c->scur].p;
@@ -1563,7 +1570,7 @@ int dpd_wall_carve(dpd_ctx *c, int32_t wall_species, int64_t *n_frozen, int64_t 
     // re-sort the survivors into cells (dt = 0) and prime F at the current step (C-2 item 2)
     const IntegP ip0 = integ(c, 0.0f, 0.0f);
     TRY(phase_bin(c, ip0, false));
-    TRY(phase_sort(c, ip0, false));
+    TRY(phase_sort(c, ip0, false, true));
     c->primed = true;
     if (c->group) {
         c->need_prime = true;
@@ -1678,7 +1685,7 @@ int dpd_set_particles_typed(dpd_ctx *c, int64_t n, const float *pos, const float
     // sort into cells without moving (dt = 0, kick = 0), then prime F_0 at s = step0
     const IntegP ip0 = integ(c, 0.0f, 0.0f);
     TRY(phase_bin(c, ip0, false));
-    TRY(phase_sort(c, ip0, false));
+    TRY(phase_sort(c, ip0, false, true));
     c->primed = true;
     if (c->group) {
         c->need_prime = true; // forces need every member's ghosts: dpd_group_step(..., 0)

@@ -95,8 +95,7 @@ __global__ void __launch_bounds__(256) k_bin_recv(Msgs rec, Geom g, int maxcap, 
 
 __global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxcap, const int *__restrict__ start,
                                                       const int *__restrict__ rank_in, float4 *__restrict__ pos_o,
-                                                      float4 *__restrict__ vel_o, float4 *__restrict__ frc_o, int cap,
-                                                      int *err)
+                                                      float4 *__restrict__ vel_o, int cap, int *err)
 {
     const int d = blockIdx.y;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -112,8 +111,7 @@ __global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxc
         return;
     }
     pos_o[dst] = p;
-    vel_o[dst] = v;
-    frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    vel_o[dst] = v; // the force slot is already zero (k_force_tile zeroes the buffer a step ahead)
 }
 
 

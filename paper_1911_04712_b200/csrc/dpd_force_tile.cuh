@@ -805,11 +805,23 @@ template <bool RECORD, int KMODE>
 __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
                  const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
-                 PairRec rec, int *err)
+                 PairRec rec, int *err, float4 *__restrict__ fzero, int nzero)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ForceTileSmem &S = *reinterpret_cast<ForceTileSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the step's other force buffer (read by this step's bin/scatter, accumulated into by the
+    // next step's force pass) is zeroed here, a slice per CTA: this kernel leaves HBM idle, so
+    // k_scatter no longer writes a zeroed force array
+#ifndef FZERO_CTAS
+#define FZERO_CTAS 444 // the first wave (3 tiles x 148 SMs): the zeroed lines age out of L2 before k_bin
+#endif
+    if (fzero) {
+        const int nb = min((int)(gridDim.x * gridDim.y * gridDim.z), FZERO_CTAS);
+        const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        if (b < nb)
+            for (int k = b * FT_NTHR + tid; k < nzero; k += nb * FT_NTHR) fzero[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
     const RoundKeys &ks = rk; // host-computed round keys of this step (constant bank)
     static_assert(FT_BZ <= 2, "home-row decoding assumes at most two home layers");
     // 3D grid: one CTA per tile, no integer division

@@ -266,7 +266,14 @@ __global__ void __launch_bounds__(256, 8) k_bin(const float4 *__restrict__ pos, 
                                              IntegP ip, int *__restrict__ count, int *__restrict__ rank, Msgs mig,
                                              int *err)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+#ifndef KBIN_REVERSE
+#define KBIN_REVERSE 1
+#endif
+    // blocks walk the particles from the high end: the force kernel just touched the high
+    // addresses last (tiles in increasing z), so they are still in L2; k_scatter then walks
+    // forward from the low end that this kernel touched last
+    const int blk = KBIN_REVERSE ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+    const int i = blk * blockDim.x + threadIdx.x;
     const int n = *n_ptr;
     int c = -1;
     if (i < n) {
@@ -444,14 +451,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, 
 }
 
 // ---------------------------------------------------------------------------------------
-// a4: scatter into cell order; recomputes a1 in registers (bit-identical to k_bin).
+// a4: scatter into cell order; recomputes a1 in registers (bit-identical to k_bin).  The
+// sorted force array it pairs with is already zero (k_force_tile zeroes it one step ahead).
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                                  const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
                                                  IntegP ip, const int *__restrict__ start,
                                                  const int *__restrict__ rank, float4 *__restrict__ pos_o,
-                                                 float4 *__restrict__ vel_o, float4 *__restrict__ frc_o, int cap,
-                                                 int *err)
+                                                 float4 *__restrict__ vel_o, int cap, int *err)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= *n_ptr || rank[i] < 0) return; // rank < 0: migrant, sent away
@@ -468,7 +475,7 @@ __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos,
     }
     pos_o[dst] = make_float4(xn.x, xn.y, xn.z, p.w);
     vel_o[dst] = make_float4(un.x, un.y, un.z, v.w); // w: species
-    frc_o[dst] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    // no force write: the target force buffer was zeroed by the previous force pass
 }
 
 // ---------------------------------------------------------------------------------------
