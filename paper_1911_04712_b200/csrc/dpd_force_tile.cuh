@@ -39,7 +39,12 @@ constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
 #endif
 constexpr int FT_NTHR = FT_NTHR_DEF;          // 9 warps: ~28 home particles each (balanced ranges)
 constexpr int FT_NWARP = FT_NTHR / 32;
-constexpr int FT_SCAP = 1024;                 // staged particles (mean 864, sd 29 at rho = 8: 5.5 sd)
+#ifndef FT_FUSED
+#define FT_FUSED 1                            // fused per-lane sweep over sentinel-separated rows
+#endif
+constexpr int FT_GAP = FT_FUSED ? 3 : 0;      // far-away sentinel slots after every staged row
+constexpr int FT_ROWPAD = FT_FUSED ? 1 : 0;   // one extra table entry per staged row: the row's end
+constexpr int FT_SCAP = FT_FUSED ? 1088 : 1024; // staged particles + 18 row gaps (mean 864 + 54, sd 29)
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
 constexpr int FT_LCAP = 40;                   // hits per home particle (mean 16.8, sd 4.1)
 constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 21 words per list (odd): conflict-free appends
@@ -50,6 +55,7 @@ constexpr int FT_NCUR = FT_NCUR_DEF;          // independent pair chains per lan
 #ifndef FT_MINB
 #define FT_MINB 3                             // resident tiles per SM (register budget)
 #endif
+constexpr float FT_FAR = 1.0e18f;             // sentinel coordinate (its r^2 ~ 3e36 stays finite)
 constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32 owners + sentinel)
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
@@ -63,9 +69,11 @@ struct FixP {
 // Cell table of one tile (SURVEY §8a row a5 staging): staged cell -> smem / global start,
 // home rows -> first home index, staged particle count.
 struct TileTab {
-    int soff[FT_NSC + 1]; // staged cell -> smem start (exclusive scan)
-    int cgs[FT_NSC];      // staged cell -> global start
+    int soff[(FT_SX + FT_ROWPAD) * FT_SY * FT_SZ + 1]; // staged cell -> smem start; with FT_ROWPAD the
+                                                       // entry after a row's last cell is the row's end
+    int cgs[(FT_SX + FT_ROWPAD) * FT_SY * FT_SZ];      // staged cell -> global start
     int hoff[FT_NHROW + 1]; // home row -> first home index (prefix)
+    int rend[FT_SY * FT_SZ]; // staged row -> end of its particles (the sentinel gap follows)
     int total;            // staged particles
 };
 
@@ -512,7 +520,7 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
     const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
     const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
     (void)x0; (void)y0; (void)z0; (void)sza;
-    const int nsc = sxa * sya * sza;
+    const int nsc = (sxa + FT_ROWPAD) * sya * sza;
     static_assert(FT_SY * FT_SZ <= 32 && FT_NHROW <= 32, "one lane per row");
     if (role == 0) {
         const int nrows = sya * sza;
@@ -538,8 +546,8 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
         }
         const int incl = warp_incl_scan(rsum, lane);
         if (lane < nrows) {
-            int run = incl - rsum;
-            const int c0 = lane * sxa;
+            int run = incl - rsum + FT_GAP * lane; // rows separated by FT_GAP sentinel slots
+            const int c0 = lane * (sxa + FT_ROWPAD);
 #pragma unroll
             for (int x = 0; x < FT_SX; ++x) {
                 if (x < sxa) {
@@ -548,8 +556,10 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
                     run += cnt[x];
                 }
             }
+            T.rend[lane] = run;
+            if (FT_ROWPAD) T.soff[c0 + sxa] = run; // segment ends never include the sentinel gap
         }
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int tot = __shfl_sync(0xffffffffu, incl, 31) + FT_GAP * nrows;
         if (lane == 0) {
             T.soff[nsc] = tot;
             T.total = tot;
@@ -582,9 +592,9 @@ __device__ __forceinline__ void tile_stage_issue(SM &S, const TileTab &T, const 
     (void)x0; (void)y0; (void)z0; (void)sza;
     const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
-        const int c0 = sxa * row; // lx = 0
+        const int c0 = (sxa + FT_ROWPAD) * row; // lx = 0
         // segment A: lx = 0; B: lx = 1..bx; C: lx = bx + 1 (merged when not wrapped)
-        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.soff[c0 + bx + 2];
+        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.rend[row];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
         if (wrap_lo) stage_copy(S, pos, vel, T.cgs[c0], a0, b0 - a0, lane);
         stage_copy(S, pos, vel, wrap_lo ? T.cgs[c0 + 1] : T.cgs[c0], mlo, mhi - mlo, lane);
@@ -607,12 +617,17 @@ __device__ __forceinline__ void tile_stage_fix(SM &S, const TileTab &T, const Ti
         const int gy = y0 - 1 + ly, gz = z0 + lz;
         const float sy = g.split[1] ? 0.0f : (gy < 0 ? -g.L[1] : (gy >= g.n[1] ? g.L[1] : 0.0f));
         const float sz = g.split[2] ? 0.0f : (gz >= g.n[2] ? g.L[2] : 0.0f);
-        const int c0 = sxa * row;
-        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.soff[c0 + bx + 2];
+        const int c0 = (sxa + FT_ROWPAD) * row;
+        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.rend[row];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
         if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
         stage_fix<KMODE>(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
         if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
+        if (lane < FT_GAP) { // sentinels: a sweep block running past a row end fails the cutoff test
+            S.sx[e0 + lane] = FT_FAR;
+            S.sy[e0 + lane] = FT_FAR;
+            S.sz[e0 + lane] = FT_FAR;
+        }
     }
 }
 
@@ -629,7 +644,8 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
     // ---- 2-4. per warp, one home particle per lane (a second round only past FT_NTHR):
     //           sweep the lane's 5 segments into its list, then evaluate the warp's pairs
     //           with a warp-balanced split -- no CTA barrier between sweep and pairs
-    const int rowz = sxa * sya;
+    const int rs = sxa + FT_ROWPAD; // table row stride
+    const int rowz = rs * sya;
     const float hx = g.L[0] / (float)g.n[0], hy = g.L[1] / (float)g.n[1], hz = g.L[2] / (float)g.n[2];
     const int wb = warp * FT_WSTRIDE;
     const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[tid * FT_LSTRIDE]);
@@ -644,12 +660,12 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             while (r + 1 < by * bz && T.hoff[r + 1] <= h) ++r;
             const int lz = r >= by ? 1 : 0;
             const int ly = 1 + r - lz * by;
-            const int crow = sxa * (ly + sya * lz);
+            const int crow = rs * (ly + sya * lz);
             s_i = T.soff[crow + 1] + (h - T.hoff[r]);
             int lx = 1;
             while (lx < bx && T.soff[crow + lx + 1] <= s_i) ++lx;
             const int c = crow + lx;
-            const int c1 = c - 1 + sxa; // (lx - 1, ly + 1, lz): the y+1 row
+            const int c1 = c - 1 + rs; // (lx - 1, ly + 1, lz): the y+1 row
             const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
             // row-end pruning: lower bounds (minus a rounding slack) on the distance from i
             // to its cell's faces; a row / end cell farther than r_c holds no partner
@@ -663,10 +679,112 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 #ifndef PROBE_NOSWEEP // timing probes: compile the sweep / pair walk out; wrong forces
 #define PROBE_NOSWEEP 0
 #endif
+#if FT_FUSED
+            // Fused sweep.  The first aligned block of segment 0 (own cell after i, next cell)
+            // is the only masked one (j > i) and is peeled: every lane runs exactly one.  All
+            // later blocks are unmasked: a block running past a segment end meets a cell two
+            // away (distance > h >= r_c) or the row's sentinels, which fail the cutoff test.
+            // The lane's remaining segments (rest of 0, then the pruned rows) are one queue,
+            // walked by one loop, so a lane's trip count is its total block count.
+            const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
+            const int a0s = s_i + 1, b0s = T.soff[c + 2];
+            const int j0 = a0s & ~3;
+            if (!PROBE_NOSWEEP && j0 < b0s) {
+                float ra, rb, rc, rd;
+                r2_quad(S, j0, PX, PY, PZ, ra, rb, rc, rd);
+                append_if_in(lptr, ra, pp.rc2, (unsigned)j0, a0s, b0s);
+                append_if_in(lptr, rb, pp.rc2, (unsigned)(j0 + 1), a0s, b0s);
+                append_if_in(lptr, rc, pp.rc2, (unsigned)(j0 + 2), a0s, b0s);
+                append_if_in(lptr, rd, pp.rc2, (unsigned)(j0 + 3), a0s, b0s);
+            }
+            // queue of non-empty segments, packed (end << 16) | aligned start, in sweep order
+            unsigned q0 = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+#pragma unroll
+            for (int k = 4; k >= 0; --k) {
+                int a, b;
+                bool ne;
+                if (k == 0) {
+                    a = j0 + 4;
+                    b = b0s;
+                    ne = a < b;
+                } else {
+                    const int cs = (k == 1) ? c1 : c1 - 2 * rs + rowz + (k - 2) * rs;
+                    const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
+                    const float qz = (k == 1) ? 0.0f : dzr;
+                    const float q = qy * qy + qz * qz;
+                    a = (dxl * dxl + q < pp.rc2) ? T.soff[cs] : T.soff[cs + 1];
+                    b = (dxr * dxr + q < pp.rc2) ? T.soff[cs + 3] : T.soff[cs + 2];
+                    ne = q < pp.rc2 && a < b;
+                }
+                if (PROBE_NOSWEEP) ne = false;
+                if (ne) {
+                    q4 = q3;
+                    q3 = q2;
+                    q2 = q1;
+                    q1 = q0;
+                    q0 = ((unsigned)b << 16) | (unsigned)(a & ~3);
+                }
+            }
+            int j = (int)(q0 & 0xFFFFu), hi = (int)(q0 >> 16);
+            q0 = q1;
+            q1 = q2;
+            q2 = q3;
+            q3 = q4;
+            q4 = 0;
+#pragma unroll 1
+            while (j < hi) {
+                if ((int)(lptr - lbase) > 2 * (FT_LCAP - 4)) { // list full (~4 sigma): the rest in place
+                    full = true;
+                    break;
+                }
+                float ra, rb, rc, rd;
+                r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
+                append_if(lptr, ra, pp.rc2, (unsigned)j);
+                append_if(lptr, rb, pp.rc2, (unsigned)(j + 1));
+                append_if(lptr, rc, pp.rc2, (unsigned)(j + 2));
+                append_if(lptr, rd, pp.rc2, (unsigned)(j + 3));
+                j += 4;
+                if (j >= hi) { // next segment (predicated pop)
+                    j = (int)(q0 & 0xFFFFu);
+                    hi = (int)(q0 >> 16);
+                    q0 = q1;
+                    q1 = q2;
+                    q2 = q3;
+                    q3 = q4;
+                    q4 = 0;
+                }
+            }
+            if (full) {
+                const float4 pi = ldp<KMODE>(S, s_i), vi = ldv<KMODE>(S, s_i);
+                for (;;) {
+                    for (; j < hi; ++j) { // candidates before a segment's start fail the cutoff test
+                        if (!(r2_one(S, j, px, py, pz) < pp.rc2)) continue;
+                        float dx, dy, dz;
+                        const float s =
+                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, j), ldv<KMODE>(S, j), ks, rec, err, dx, dy, dz);
+                        const int qx = fix_q(dx, s), qy = fix_q(dy, s), qz = fix_q(dz, s);
+                        atomicAdd(&S.acc[0][s_i], qx);
+                        atomicAdd(&S.acc[1][s_i], qy);
+                        atomicAdd(&S.acc[2][s_i], qz);
+                        atomicAdd(&S.acc[0][j], -qx);
+                        atomicAdd(&S.acc[1][j], -qy);
+                        atomicAdd(&S.acc[2][j], -qz);
+                    }
+                    if (q0 == 0) break;
+                    j = (int)(q0 & 0xFFFFu);
+                    hi = (int)(q0 >> 16);
+                    q0 = q1;
+                    q1 = q2;
+                    q2 = q3;
+                    q3 = q4;
+                    q4 = 0;
+                }
+            }
+#else
 #pragma unroll // all five segments (measured 457 -> 449 us against a rolled loop)
             for (int k = 0; k < (PROBE_NOSWEEP ? 0 : 5); ++k) {
                 // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
-                const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * sxa + rowz + (k - 2) * sxa);
+                const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * rs + rowz + (k - 2) * rs);
                 int a = (k == 0) ? s_i + 1 : T.soff[cs];
                 int b = T.soff[cs + (k == 0 ? 2 : 3)];
                 if (k > 0) {
@@ -707,6 +825,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                     }
                 }
             }
+#endif
             if (full) atomicAdd(&err[6], 1); // statistics: in-place evaluations
             cnt = (int)(lptr - lbase) >> 1;
         }
@@ -781,8 +900,8 @@ __device__ __forceinline__ void tile_flush(const SM &S, const TileTab &T, const 
     (void)x0; (void)y0; (void)z0; (void)sza;
     const bool wrap_lo = !g.split[0] && x0 == 0, wrap_hi = !g.split[0] && x0 + bx == g.n[0];
     for (int row = warp; row < sya * sza; row += FT_NWARP) {
-        const int c0 = sxa * row;
-        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.soff[c0 + bx + 2];
+        const int c0 = (sxa + FT_ROWPAD) * row;
+        const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.rend[row];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
         const int gm = wrap_lo ? T.cgs[c0 + 1] : T.cgs[c0];
         for (int s = a0 + lane; s < e0; s += 32) {
