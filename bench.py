@@ -496,6 +496,18 @@ def main():
             roof["traffic_source"] = tsrc
             roof["traffic_vs_algorithmic"] = t["dram_bytes"] / (48.0 * n_local) if dom == "force" else \
                 t["dram_bytes"] / max(1.0, KERNEL_BYTES.get(dom, 0.0) * n_local)
+            if dom == "force" and t.get("smem_wavefronts"):
+                # the co-limiting resource of the force kernel: shared-memory
+                # wavefronts of the ncu capture over this run's launch time, against one
+                # wavefront per cycle per SM
+                clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+                sec = per_kernel[dom]["ms_per_launch"] * 1e-3
+                wf = float(t["smem_wavefronts"])
+                roof["smem_view"] = {"wavefronts_per_launch": wf, "achieved_wf_per_s": wf / sec,
+                                     "peak_wf_per_s": 148 * clk, "frac": wf / sec / (148 * clk),
+                                     "warp_instr_per_launch": t.get("warp_instr"),
+                                     "issue_frac": (t["warp_instr"] / sec / (148 * 4 * clk)) if t.get("warp_instr") else None,
+                                     "peak_source": "148 SM x 1 shared wavefront/cycle x sm_max_mhz"}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,

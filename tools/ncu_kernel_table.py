@@ -21,6 +21,8 @@ METRICS = OrderedDict([
     ("lts__t_sectors_op_red.sum", "l2_red_sectors"),
     ("lts__t_sectors_op_atom.sum", "l2_atom_sectors"),
     ("smsp__sass_inst_executed_op_shared_atom.sum", "smem_atom_instr"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem_wf_pct"),
     ("smsp__inst_executed.sum", "warp_instr"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "lanes_per_instr"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_pct"),
@@ -63,16 +65,16 @@ def main():
                 x *= SCALE[u]  # -> bytes
             a[key] = a.get(key, 0.0) + x
     print("| kernel | launches | time us | DRAM MB (r+w) | DRAM % peak | L2 hit % | L1 hit % | L2 red sectors | "
-          "L2 atom sectors | smem atomics (warp-instr) | warp-instr | lanes/instr | issue active % | warps active % |"
-          + (" lane-instr / particle |" if n else ""))
-    print("|---" * (14 + (1 if n else 0)) + "|")
+          "L2 atom sectors | smem atomics (warp-instr) | smem wavefronts | smem wf % peak | warp-instr | lanes/instr | "
+          "issue active % | warps active % |" + (" lane-instr / particle |" if n else ""))
+    print("|---" * (16 + (1 if n else 0)) + "|")
     for name, a in acc.items():
         k = a["launches"]
         g = lambda key, d=0.0: a.get(key, d) / k  # noqa: E731
         row = [name, str(k), f"{g('time'):.1f}", f"{(g('dram_read') + g('dram_write')) / 1e6:.1f}",
                f"{g('dram_pct'):.1f}", f"{g('l2_hit_pct'):.1f}", f"{g('l1_hit_pct'):.1f}",
                f"{g('l2_red_sectors'):.3g}", f"{g('l2_atom_sectors'):.3g}", f"{g('smem_atom_instr'):.3g}",
-               f"{g('warp_instr'):.3g}", f"{g('lanes_per_instr'):.1f}", f"{g('issue_active_pct'):.1f}",
+               f"{g('smem_wavefronts'):.3g}", f"{g('smem_wf_pct'):.1f}", f"{g('warp_instr'):.3g}", f"{g('lanes_per_instr'):.1f}", f"{g('issue_active_pct'):.1f}",
                f"{g('warps_active_pct'):.1f}"]
         if n:
             row.append(f"{g('warp_instr') * g('lanes_per_instr') / n:.0f}")

@@ -2,7 +2,8 @@
 
 usage: python tools/ncu_traffic.py report.ncu-rep out.json workload n_local
 Maps kernel names to bench keys (force, bin, scan, scatter) and records
-dram__bytes_read.sum + dram__bytes_write.sum and gpu__time_duration.sum per launch
+dram__bytes_read.sum + dram__bytes_write.sum, gpu__time_duration.sum, shared-memory
+wavefronts and executed warp-instructions per launch
 (averaged over the captured launches of that kernel)."""
 import csv
 import io
@@ -19,7 +20,8 @@ UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, 
 def main():
     rep, out = sys.argv[1], sys.argv[2]
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                          "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum,smsp__inst_executed.sum"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -32,10 +34,13 @@ def main():
         if key is None:
             continue
         vals = {}
-        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                  "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum"):
             vals[m] = float(r[col[m]].replace(",", "")) * UNIT.get(units[col[m]], 1.0)
         a = acc.setdefault(key, {"launches": 0, "bytes": 0.0, "read": 0.0, "write": 0.0, "time_s": 0.0,
-                                 "kernel": name.split("(")[0]})
+                                 "wf": 0.0, "instr": 0.0, "kernel": name.split("(")[0]})
+        a["wf"] += vals["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
+        a["instr"] += vals["smsp__inst_executed.sum"]
         a["launches"] += 1
         a["read"] += vals["dram__bytes_read.sum"]
         a["write"] += vals["dram__bytes_write.sum"]
@@ -46,6 +51,7 @@ def main():
         n = a["launches"]
         res["per_launch"][k] = {"kernel": a["kernel"], "dram_bytes": a["bytes"] / n, "dram_read": a["read"] / n,
                                 "dram_write": a["write"] / n, "ncu_time_us": 1e6 * a["time_s"] / n,
+                                "smem_wavefronts": a["wf"] / n, "warp_instr": a["instr"] / n,
                                 "launches_captured": n, "workload": sys.argv[3], "n_local": int(sys.argv[4])}
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
