@@ -517,3 +517,45 @@ def test_full_size_sampled_parity_other_configs(name):
     _, ocount, ostart = oracle.cells(p, by_id(ids, pos)[0])
     assert np.array_equal(count, ocount) and np.array_equal(start, ostart)
     assert np.abs(F.astype(np.float64).sum(0)).max() < 1e-5 * np.abs(F).sum()
+
+
+# Boxes whose x extent leaves a partial last tile (1-3 home cells wide), so segment ends meet
+# row ends at every tile width the staging produces (DESIGN §6 step 3: sentinel gaps).
+PAIRSET_BOXES = [(11.3, 9.7, 7.2), (17.0, 13.0, 6.0), (9.0, 6.0, 5.0), (8.0, 8.0, 8.0), (3.5, 17.0, 5.0)]
+
+
+@pytest.mark.parametrize("box", PAIRSET_BOXES)
+def test_tiled_pair_set_equals_reference_kernel(box):
+    """The tiled kernel's fused sweep tests whole 4-candidate blocks past segment ends and relies
+    on geometry (cells two apart are farther than r_c) and per-row sentinels to reject them.
+    The pair set it evaluates must equal the reference thread-per-particle kernel's exactly on
+    the same state (no duplicate, none missing), up to pairs inside the fp32 cutoff window,
+    over 40 steps of rho = 8."""
+    cfg = workloads.Config("pairset", box, 8.0, 25.0, 4.5, 1.0, 0.5, 0.005)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg, kernel=0)
+    d.set_particles(pos0, vel0)
+    L = np.array(cfg.box)
+    for s in range(41):
+        if s % 10 == 0:
+            sets = []
+            for kern in (0, 1):
+                d.set_option("force_kernel", kern)
+                q = d.debug_pairs()
+                key = q[:, 0].astype(np.int64) * (1 << 32) + q[:, 1].astype(np.int64)
+                assert len(np.unique(key)) == len(key), f"kernel {kern}: duplicate pair at step {s}"
+                sets.append(key)
+            d.set_option("force_kernel", 0)
+            diff = np.setxor1d(sets[0], sets[1])
+            if diff.size:
+                pos, _, _, ids = d.get_state()
+                x = np.empty_like(pos, dtype=np.float64)
+                x[ids] = pos
+                a, b = diff >> 32, diff & 0xFFFFFFFF
+                dr = x[a] - x[b]
+                dr -= L * np.round(dr / L)
+                r2 = (dr * dr).sum(axis=1)
+                assert np.all(np.abs(r2 - cfg.rc ** 2) < 1e-4), \
+                    f"step {s}: {diff.size} pairs differ away from the cutoff (r2 = {r2[:5]})"
+        if s < 40:
+            d.step(1)
