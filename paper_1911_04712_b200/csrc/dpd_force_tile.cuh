@@ -699,8 +699,15 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             }
             // queue of non-empty segments, packed (end << 16) | aligned start, in sweep order
             unsigned q0 = 0, q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+#ifndef FT_LOCKSTEP
+#define FT_LOCKSTEP 1
+#endif
 #pragma unroll
-            for (int k = 4; k >= 0; --k) {
+            for (int kk = 0; kk < 5; ++kk) {
+                // push-front order: FT_LOCKSTEP walks the four rows first, unpruned, so lanes
+                // of one cell read the same candidate quads together (shared-memory broadcast),
+                // and their own-cell rest last; else own-cell rest first, rows pruned
+                const int k = FT_LOCKSTEP ? (kk == 0 ? 0 : 5 - kk) : 4 - kk;
                 int a, b;
                 bool ne;
                 if (k == 0) {
@@ -712,9 +719,9 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                     const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
                     const float qz = (k == 1) ? 0.0f : dzr;
                     const float q = qy * qy + qz * qz;
-                    a = (dxl * dxl + q < pp.rc2) ? T.soff[cs] : T.soff[cs + 1];
-                    b = (dxr * dxr + q < pp.rc2) ? T.soff[cs + 3] : T.soff[cs + 2];
-                    ne = q < pp.rc2 && a < b;
+                    a = (FT_LOCKSTEP || dxl * dxl + q < pp.rc2) ? T.soff[cs] : T.soff[cs + 1];
+                    b = (FT_LOCKSTEP || dxr * dxr + q < pp.rc2) ? T.soff[cs + 3] : T.soff[cs + 2];
+                    ne = (FT_LOCKSTEP || q < pp.rc2) && a < b;
                 }
                 if (PROBE_NOSWEEP) ne = false;
                 if (ne) {
