@@ -33,6 +33,9 @@ namespace dpd {
 constexpr int FT_BX = 4, FT_BY = 4, FT_BZ = 2;
 constexpr int FT_SX = FT_BX + 2, FT_SY = FT_BY + 2, FT_SZ = FT_BZ + 1;
 constexpr int FT_NSC = FT_SX * FT_SY * FT_SZ; // staged cells (108)
+#ifndef FT_GRED
+#define FT_GRED 0 // 1: pair forces in fp32 straight to the global force array (RED.F32x4), no shared sums
+#endif
 constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
 #ifndef FT_NTHR_DEF
 #define FT_NTHR_DEF 288
@@ -82,7 +85,11 @@ struct ForceTileSmem {
     unsigned short lst[FT_NTHR * FT_LSTRIDE]; // per-thread pair lists (one home particle each);
                                               // during staging: the AoS landing buffer of the positions
     float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // staged positions (tile frame), SoA
+#if FT_GRED
+    int gidx[FT_SCAP];                           // staged particle -> its global (sorted) index
+#else
     int acc[3][FT_SCAP];                         // fixed-point force sums
+#endif
     int4 wrec[FT_NWARP * FT_WSTRIDE];            // per warp, compacted owners: {list prefix, prefix + count,
                                                  //   list base minus prefix, staged index} (one LDS.128)
     TileTab tab[1];                              // the tile's cell table
@@ -140,6 +147,18 @@ __device__ __forceinline__ int fix_q(float d, float s)
 {
     return __float_as_int(__fmaf_rn(d, s, 12582912.0f)) - 0x4B400000;
 }
+
+// Pair-force accumulation.  Default: 32-bit fixed point in shared memory (exact Newton-3,
+// order-independent tile sums, flushed once per staged particle).  FT_GRED: fp32 forces
+// reduced straight into the global force array (RED.E.ADD.F32x4), no shared sums and no
+// flush barrier.
+#if FT_GRED
+using AccT = float;
+__device__ __forceinline__ AccT acc_q(float d, float s) { return d * s; }
+#else
+using AccT = int;
+__device__ __forceinline__ AccT acc_q(float d, float s) { return fix_q(d, s); }
+#endif
 
 __device__ __forceinline__ int to_fixed(float f, float scale)
 {
@@ -200,6 +219,16 @@ __device__ __forceinline__ void append_if_lt(unsigned &lptr, float r2, float rc2
                  "@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
                  : "+r"(lptr)
                  : "f"(r2), "f"(rc2), "r"(j), "r"(hi)
+                 : "memory");
+}
+
+// Append j if r2 < rc2 and j > jmin (the lockstep own-cell sweep: only partners after i).
+__device__ __forceinline__ void append_if_gt(unsigned &lptr, float r2, float rc2, unsigned j, int jmin)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tsetp.gt.and.s32 p, %3, %4, p;\n\t"
+                 "@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
+                 : "+r"(lptr)
+                 : "f"(r2), "f"(rc2), "r"(j), "r"(jmin)
                  : "memory");
 }
 
@@ -281,7 +310,7 @@ __device__ __forceinline__ void stage_copy(SM &S, const float4 *__restrict__ pos
 // Second pass over a staged range: periodic-image shift, SoA copy, id (| species << 30) into
 // the velocity word, zeroed accumulators.
 template <int KMODE, class SM>
-__device__ __forceinline__ void stage_fix(SM &S, int s0, int len, float sx, float sy, float sz, int lane)
+__device__ __forceinline__ void stage_fix(SM &S, int s0, int len, int g0, float sx, float sy, float sz, int lane)
 {
     for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
@@ -292,9 +321,14 @@ __device__ __forceinline__ void stage_fix(SM &S, int s0, int len, float sx, floa
         uint32_t word = __float_as_uint(p.w);
         if constexpr (KMODE == 3) word |= (uint32_t)__float_as_int(S.sv[s].w) << 30;
         S.sv[s].w = __uint_as_float(word);
+#if FT_GRED
+        S.gidx[s] = g0 + k;
+#else
+        (void)g0;
         S.acc[0][s] = 0;
         S.acc[1][s] = 0;
         S.acc[2][s] = 0;
+#endif
     }
 }
 
@@ -380,8 +414,21 @@ struct PairCursor {
     int t, t1, o, enext, si, lrow;
     float px, py, pz;
     float4 vi;
-    int fx, fy, fz;
+    AccT fx, fy, fz;
 };
+
+// Add (x, y, z) to staged particle s's force.
+__device__ __forceinline__ void acc_add(ForceTileSmem &S, float4 *frc, int s, AccT x, AccT y, AccT z)
+{
+#if FT_GRED
+    atomicAdd(&frc[S.gidx[s]], make_float4(x, y, z, 0.0f));
+#else
+    (void)frc;
+    atomicAdd(&S.acc[0][s], x); // native ATOMS.ADD (the fp32 variant is a CAS loop)
+    atomicAdd(&S.acc[1][s], y);
+    atomicAdd(&S.acc[2][s], z);
+#endif
+}
 
 __device__ __forceinline__ void cursor_load(PairCursor &c, const ForceTileSmem &S)
 {
@@ -408,37 +455,31 @@ __device__ __forceinline__ void cursor_init(PairCursor &c, const ForceTileSmem &
     cursor_load(c, S);
 }
 
-__device__ __forceinline__ void cursor_flush(PairCursor &c, ForceTileSmem &S)
+__device__ __forceinline__ void cursor_flush(PairCursor &c, ForceTileSmem &S, float4 *frc)
 {
-    if (c.fx | c.fy | c.fz) {
-        atomicAdd(&S.acc[0][c.si], c.fx);
-        atomicAdd(&S.acc[1][c.si], c.fy);
-        atomicAdd(&S.acc[2][c.si], c.fz);
-    }
+    if (c.fx != 0 || c.fy != 0 || c.fz != 0) acc_add(S, frc, c.si, c.fx, c.fy, c.fz);
     c.fx = c.fy = c.fz = 0;
 }
 
 // Entry t of the list (the partner j); moves to the next owner first when t crosses it.
-__device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S)
+__device__ __forceinline__ int cursor_next(PairCursor &c, ForceTileSmem &S, float4 *frc)
 {
     if (c.t >= c.enext) { // next owner (never empty)
-        cursor_flush(c, S);
+        cursor_flush(c, S, frc);
         ++c.o;
         cursor_load(c, S);
     }
     return S.lst[c.lrow + c.t];
 }
 
-__device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &S, int j, float s, float dx, float dy,
-                                                  float dz, float scale)
+__device__ __forceinline__ void cursor_accumulate(PairCursor &c, ForceTileSmem &S, float4 *frc, int j, float s,
+                                                  float dx, float dy, float dz)
 {
-    const int qx = fix_q(dx, s), qy = fix_q(dy, s), qz = fix_q(dz, s);
+    const AccT qx = acc_q(dx, s), qy = acc_q(dy, s), qz = acc_q(dz, s);
     c.fx += qx;
     c.fy += qy;
     c.fz += qz;
-    atomicAdd(&S.acc[0][j], -qx); // native ATOMS.ADD (the fp32 variant is a CAS loop)
-    atomicAdd(&S.acc[1][j], -qy);
-    atomicAdd(&S.acc[2][j], -qz);
+    acc_add(S, frc, j, -qx, -qy, -qz);
     ++c.t;
 }
 
@@ -620,9 +661,9 @@ __device__ __forceinline__ void tile_stage_fix(SM &S, const TileTab &T, const Ti
         const int c0 = (sxa + FT_ROWPAD) * row;
         const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.rend[row];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
-        if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
-        stage_fix<KMODE>(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
-        if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
+        if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, T.cgs[c0], -g.L[0], sy, sz, lane);
+        stage_fix<KMODE>(S, mlo, mhi - mlo, wrap_lo ? T.cgs[c0 + 1] : T.cgs[c0], 0.0f, sy, sz, lane);
+        if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, T.cgs[c0 + bx + 1], g.L[0], sy, sz, lane);
         if (lane < FT_GAP) { // sentinels: a sweep block running past a row end fails the cutoff test
             S.sx[e0 + lane] = FT_FAR;
             S.sy[e0 + lane] = FT_FAR;
@@ -635,7 +676,7 @@ __device__ __forceinline__ void tile_stage_fix(SM &S, const TileTab &T, const Ti
 template <bool RECORD, int KMODE>
 __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, const TileGeo &G, const Geom &g,
                                            const PairP &pp, const FixP &fx, const RoundKeys &ks, PairRec &rec,
-                                           int *err, int tid, int warp, int lane)
+                                           int *err, float4 *frc, int tid, int warp, int lane)
 {
     const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
     const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
@@ -689,7 +730,10 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
             const int a0s = s_i + 1, b0s = T.soff[c + 2];
             const int j0 = a0s & ~3;
-            if (!PROBE_NOSWEEP && j0 < b0s) {
+#ifndef FT_SEG0LOCK
+#define FT_SEG0LOCK 0
+#endif
+            if (!FT_SEG0LOCK && !PROBE_NOSWEEP && j0 < b0s) {
                 float ra, rb, rc, rd;
                 r2_quad(S, j0, PX, PY, PZ, ra, rb, rc, rd);
                 append_if_in(lptr, ra, pp.rc2, (unsigned)j0, a0s, b0s);
@@ -713,7 +757,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 if (k == 0) {
                     a = j0 + 4;
                     b = b0s;
-                    ne = a < b;
+                    ne = !FT_SEG0LOCK && a < b; // FT_SEG0LOCK: the own cell runs after the rows
                 } else {
                     const int cs = (k == 1) ? c1 : c1 - 2 * rs + rowz + (k - 2) * rs;
                     const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
@@ -769,13 +813,9 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                         float dx, dy, dz;
                         const float s =
                             pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, j), ldv<KMODE>(S, j), ks, rec, err, dx, dy, dz);
-                        const int qx = fix_q(dx, s), qy = fix_q(dy, s), qz = fix_q(dz, s);
-                        atomicAdd(&S.acc[0][s_i], qx);
-                        atomicAdd(&S.acc[1][s_i], qy);
-                        atomicAdd(&S.acc[2][s_i], qz);
-                        atomicAdd(&S.acc[0][j], -qx);
-                        atomicAdd(&S.acc[1][j], -qy);
-                        atomicAdd(&S.acc[2][j], -qz);
+                        const AccT qx = acc_q(dx, s), qy = acc_q(dy, s), qz = acc_q(dz, s);
+                        acc_add(S, frc, s_i, qx, qy, qz);
+                        acc_add(S, frc, j, -qx, -qy, -qz);
                     }
                     if (q0 == 0) break;
                     j = (int)(q0 & 0xFFFFu);
@@ -787,6 +827,40 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                     q4 = 0;
                 }
             }
+#if FT_SEG0LOCK
+            // own cell A and A + x after the rows: every lane of A sweeps A's whole range at the
+            // same iteration (shared-memory broadcast), keeping only j > i
+            if (!PROBE_NOSWEEP) {
+                j = T.soff[c] & ~3;
+                if (!full) {
+#pragma unroll 1
+                    for (; j < b0s; j += 4) {
+                        if ((int)(lptr - lbase) > 2 * (FT_LCAP - 4)) {
+                            full = true;
+                            break;
+                        }
+                        float ra, rb, rc, rd;
+                        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
+                        append_if_gt(lptr, ra, pp.rc2, (unsigned)j, s_i);
+                        append_if_gt(lptr, rb, pp.rc2, (unsigned)(j + 1), s_i);
+                        append_if_gt(lptr, rc, pp.rc2, (unsigned)(j + 2), s_i);
+                        append_if_gt(lptr, rd, pp.rc2, (unsigned)(j + 3), s_i);
+                    }
+                }
+                if (full) {
+                    const float4 pi = ldp<KMODE>(S, s_i), vi = ldv<KMODE>(S, s_i);
+                    for (j = max(j, a0s); j < b0s; ++j) {
+                        if (!(r2_one(S, j, px, py, pz) < pp.rc2)) continue;
+                        float dx, dy, dz;
+                        const float s =
+                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, j), ldv<KMODE>(S, j), ks, rec, err, dx, dy, dz);
+                        const AccT qx = acc_q(dx, s), qy = acc_q(dy, s), qz = acc_q(dz, s);
+                        acc_add(S, frc, s_i, qx, qy, qz);
+                        acc_add(S, frc, j, -qx, -qy, -qz);
+                    }
+                }
+            }
+#endif
 #else
 #pragma unroll // all five segments (measured 457 -> 449 us against a rolled loop)
             for (int k = 0; k < (PROBE_NOSWEEP ? 0 : 5); ++k) {
@@ -822,13 +896,9 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                         float dx, dy, dz;
                         const float s =
                             pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, a), ldv<KMODE>(S, a), ks, rec, err, dx, dy, dz);
-                        const int qx = fix_q(dx, s), qy = fix_q(dy, s), qz = fix_q(dz, s);
-                        atomicAdd(&S.acc[0][s_i], qx);
-                        atomicAdd(&S.acc[1][s_i], qy);
-                        atomicAdd(&S.acc[2][s_i], qz);
-                        atomicAdd(&S.acc[0][a], -qx);
-                        atomicAdd(&S.acc[1][a], -qy);
-                        atomicAdd(&S.acc[2][a], -qz);
+                        const AccT qx = acc_q(dx, s), qy = acc_q(dy, s), qz = acc_q(dz, s);
+                        acc_add(S, frc, s_i, qx, qy, qz);
+                        acc_add(S, frc, a, -qx, -qy, -qz);
                     }
                 }
             }
@@ -869,7 +939,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 #pragma unroll
                 for (int k = 0; k < FT_NCUR; ++k) {
                     act[k] = (k == 0) || cu[k].t < cu[k].t1;
-                    j[k] = act[k] ? cursor_next(cu[k], S) : cu[k].si; // idle: self pair, r2 = 0 -> f = 0
+                    j[k] = act[k] ? cursor_next(cu[k], S, frc) : cu[k].si; // idle: self pair, r2 = 0 -> f = 0
                 }
                 float4 vj[FT_NCUR];
                 float sv_[FT_NCUR], dx[FT_NCUR], dy[FT_NCUR], dz[FT_NCUR];
@@ -886,11 +956,13 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 }
 #pragma unroll
                 for (int k = 0; k < FT_NCUR; ++k)
-                    cursor_accumulate(cu[k], S, j[k], sv_[k], dx[k], dy[k], dz[k], fx.scale); // idle: adds zeros
+                    cursor_accumulate(cu[k], S, frc, j[k], sv_[k], dx[k], dy[k], dz[k]); // idle: adds zeros
             }
 #pragma unroll
-            for (int k = 0; k < FT_NCUR; ++k) cursor_flush(cu[k], S);
-            if (amax > fx.mag_lim * fx.scale) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(cu[0].vi.w));
+            for (int k = 0; k < FT_NCUR; ++k) cursor_flush(cu[k], S, frc);
+            // fixed point: one pair must stay below 2^21 units; fp32 (FT_GRED): only non-finite
+            if (FT_GRED ? !(amax <= 3.0e38f) : amax > fx.mag_lim * fx.scale)
+                raise_err(err, ERR_RANGE, (int)w_id<KMODE>(cu[0].vi.w));
         }
         __syncwarp(); // the lists and the owner table are rewritten by the next round
     }
@@ -964,7 +1036,7 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     if (tile_overflows(T, G)) {
         if (tid == 0) atomicAdd(&err[T.total > FT_SCAP ? 4 : 5], 1); // fallback statistics
         tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, G.x0, G.y0, G.z0, G.bx, G.by,
-                                     G.bz, fx.inv_scale);
+                                     G.bz, FT_GRED ? 1.0f : fx.inv_scale);
         return;
     }
     tile_stage_issue(S, T, G, g, pos, vel, warp, lane);
@@ -972,9 +1044,11 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     __syncwarp();
     tile_stage_fix<KMODE>(S, T, G, g, warp, lane);
     __syncthreads();
-    tile_pairs<RECORD, KMODE>(S, T, G, g, pp, fx, ks, rec, err, tid, warp, lane);
+    tile_pairs<RECORD, KMODE>(S, T, G, g, pp, fx, ks, rec, err, frc, tid, warp, lane);
+#if !FT_GRED
     __syncthreads();
     tile_flush(S, T, G, g, fx, frc, warp, lane);
+#endif
 }
 
 } // namespace dpd
