@@ -494,7 +494,7 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         const FixP fx = c->fix;
         // the tiled kernel works in fixed-point units: a, gamma, sigma/sqrt(dt) pre-multiplied
         // by the power-of-two scale (exact), so one FFMA per component quantises
-        const PairP pp = FT_GRED ? c->pp : scaled_pair(c->pp, fx.scale); // FT_GRED accumulates fp32 forces
+        const PairP pp = scaled_pair(c->pp, fx.scale);
         const RoundKeys rk = host_round_keys(s_lo, s_hi, c->pp);
         const dim3 tgrid((g.n[0] + FT_BX - 1) / FT_BX, (g.n[1] + FT_BY - 1) / FT_BY, (g.n[2] + FT_BZ - 1) / FT_BZ);
         const size_t smem = sizeof(ForceTileSmem);

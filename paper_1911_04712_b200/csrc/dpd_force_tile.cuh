@@ -1,18 +1,22 @@
 // dpd_force_tile.cuh -- production pair-force sweep for sm_100a.
 //
 // One CTA of 9 warps per tile of BX x BY x BZ home cells (cell lists, symmetric
-// forces), 3 tiles resident per SM (73 KB shared memory, 72 registers); launched on a 3D grid,
+// forces), 3 tiles resident per SM (74 KB shared memory, 72 registers); launched on a 3D grid,
 // one CTA per tile:
 //   1. table   : one warp loads the staged cell table of the forward half-stencil region,
-//                (BX+2) x (BY+2) x (BZ+1) cells, straight from the cell starts and scans it;
-//                another warp scans the home rows;
+//                (BX+2) x (BY+2) x (BZ+1) cells, straight from the cell starts and scans it
+//                (one extra entry per row: the row's end); another warp scans the home rows;
 //   2. stage   : every staged row (<= 3 contiguous global ranges) is copied with cp.async.cg,
 //                then shifted to the periodic image in the tile frame and split into SoA
-//                x, y, z; the particle id rides in the staged velocity's w word;
-//   3. sweep   : one home particle per lane sweeps its 5 contiguous smem segments (own cell
-//                after i + next cell, the y+1 row, three z+1 rows; row ends beyond r_c
-//                pruned) in 4-aligned blocks -- one LDS.128 per coordinate, packed fp32x2
-//                distance math (FADD2/FFMA2), one predicated 16-bit store + add per hit;
+//                x, y, z; the particle id rides in the staged velocity's w word; every row is
+//                followed by FT_GAP far-away sentinels;
+//   3. sweep   : one home particle per lane; its first own-cell block (masked, j > i) is
+//                peeled, then one loop walks a queue of its segments -- the y+1 row and the
+//                three z+1 rows first (lanes of one cell in lockstep: their candidate quads
+//                are the same shared-memory addresses), the rest of the own cell last -- in
+//                unmasked 4-aligned blocks: a block running past a segment meets cells two
+//                away or sentinels, both beyond r_c.  One LDS.128 per coordinate, packed
+//                fp32x2 distance math (FADD2/FFMA2), one predicated 16-bit store + add per hit;
 //   4. pairs   : the warp's lists are concatenated and cut into 32 contiguous lane chunks,
 //                each walked by two cursors (two Philox/Box-Muller chains in flight); the
 //                i-side sum stays in registers until the owner changes;
@@ -33,21 +37,16 @@ namespace dpd {
 constexpr int FT_BX = 4, FT_BY = 4, FT_BZ = 2;
 constexpr int FT_SX = FT_BX + 2, FT_SY = FT_BY + 2, FT_SZ = FT_BZ + 1;
 constexpr int FT_NSC = FT_SX * FT_SY * FT_SZ; // staged cells (108)
-#ifndef FT_GRED
-#define FT_GRED 0 // 1: pair forces in fp32 straight to the global force array (RED.F32x4), no shared sums
-#endif
+
 constexpr int FT_NHROW = FT_BY * FT_BZ;       // home rows (8)
 #ifndef FT_NTHR_DEF
 #define FT_NTHR_DEF 288
 #endif
 constexpr int FT_NTHR = FT_NTHR_DEF;          // 9 warps: ~28 home particles each (balanced ranges)
 constexpr int FT_NWARP = FT_NTHR / 32;
-#ifndef FT_FUSED
-#define FT_FUSED 1                            // fused per-lane sweep over sentinel-separated rows
-#endif
-constexpr int FT_GAP = FT_FUSED ? 3 : 0;      // far-away sentinel slots after every staged row
-constexpr int FT_ROWPAD = FT_FUSED ? 1 : 0;   // one extra table entry per staged row: the row's end
-constexpr int FT_SCAP = FT_FUSED ? 1088 : 1024; // staged particles + 18 row gaps (mean 864 + 54, sd 29)
+constexpr int FT_GAP = 3;                     // far-away sentinel slots after every staged row
+constexpr int FT_ROWPAD = 1;                  // one extra table entry per staged row: the row's end
+constexpr int FT_SCAP = 1088;                 // staged particles + 18 row gaps (mean 864 + 54, sd 29)
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
 constexpr int FT_LCAP = 40;                   // hits per home particle (mean 16.8, sd 4.1)
 constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 21 words per list (odd): conflict-free appends
@@ -85,11 +84,7 @@ struct ForceTileSmem {
     unsigned short lst[FT_NTHR * FT_LSTRIDE]; // per-thread pair lists (one home particle each);
                                               // during staging: the AoS landing buffer of the positions
     float sx[FT_SCAP], sy[FT_SCAP], sz[FT_SCAP]; // staged positions (tile frame), SoA
-#if FT_GRED
-    int gidx[FT_SCAP];                           // staged particle -> its global (sorted) index
-#else
     int acc[3][FT_SCAP];                         // fixed-point force sums
-#endif
     int4 wrec[FT_NWARP * FT_WSTRIDE];            // per warp, compacted owners: {list prefix, prefix + count,
                                                  //   list base minus prefix, staged index} (one LDS.128)
     TileTab tab[1];                              // the tile's cell table
@@ -148,17 +143,11 @@ __device__ __forceinline__ int fix_q(float d, float s)
     return __float_as_int(__fmaf_rn(d, s, 12582912.0f)) - 0x4B400000;
 }
 
-// Pair-force accumulation.  Default: 32-bit fixed point in shared memory (exact Newton-3,
-// order-independent tile sums, flushed once per staged particle).  FT_GRED: fp32 forces
-// reduced straight into the global force array (RED.E.ADD.F32x4), no shared sums and no
-// flush barrier.
-#if FT_GRED
-using AccT = float;
-__device__ __forceinline__ AccT acc_q(float d, float s) { return d * s; }
-#else
+// Pair-force accumulation: 32-bit fixed point in shared memory (exact Newton-3, order-
+// independent tile sums, flushed once per staged particle; DESIGN §6.1 measures the fp32
+// global-reduction alternative).
 using AccT = int;
 __device__ __forceinline__ AccT acc_q(float d, float s) { return fix_q(d, s); }
-#endif
 
 __device__ __forceinline__ int to_fixed(float f, float scale)
 {
@@ -212,26 +201,6 @@ __device__ __forceinline__ float r2_one(const ForceTileSmem &S, int j, float px,
     return dx * dx + dy * dy + dz * dz;
 }
 
-// Append j if r2 < rc2 and j < hi (the masked tail block of the sweep).
-__device__ __forceinline__ void append_if_lt(unsigned &lptr, float r2, float rc2, unsigned j, int hi)
-{
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tsetp.lt.and.s32 p, %3, %4, p;\n\t"
-                 "@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
-                 : "+r"(lptr)
-                 : "f"(r2), "f"(rc2), "r"(j), "r"(hi)
-                 : "memory");
-}
-
-// Append j if r2 < rc2 and j > jmin (the lockstep own-cell sweep: only partners after i).
-__device__ __forceinline__ void append_if_gt(unsigned &lptr, float r2, float rc2, unsigned j, int jmin)
-{
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\tsetp.gt.and.s32 p, %3, %4, p;\n\t"
-                 "@p st.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, 2;\n\t}"
-                 : "+r"(lptr)
-                 : "f"(r2), "f"(rc2), "r"(j), "r"(jmin)
-                 : "memory");
-}
-
 // Append j if r2 < rc2 and lo <= j < hi (the masked end blocks of the aligned sweep).
 __device__ __forceinline__ void append_if_in(unsigned &lptr, float r2, float rc2, unsigned j, int lo, int hi)
 {
@@ -251,40 +220,6 @@ __device__ __forceinline__ void r2_quad(const ForceTileSmem &S, int j, unsigned 
     const ulonglong2 Z = *reinterpret_cast<const ulonglong2 *>(&S.sz[j]);
     r2_pair(X.x, Y.x, Z.x, PX, PY, PZ, ra, rb);
     r2_pair(X.y, Y.y, Z.y, PX, PY, PZ, rc, rd);
-}
-
-// Sweep of one contiguous smem segment [lo, hi): append every in-cutoff j.
-__device__ __forceinline__ void sweep(const ForceTileSmem &S, unsigned &lptr, int lo, int hi, float px, float py,
-                                      float pz, float rc2)
-{
-    // 4-aligned blocks (LDS.128 per coordinate); the first and last blocks masked to [lo, hi)
-    // (reads outside the segment stay inside the shared struct)
-    const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
-    int j = lo & ~3;
-    float ra, rb, rc, rd;
-    if (j < hi) {
-        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
-        append_if_in(lptr, ra, rc2, (unsigned)j, lo, hi);
-        append_if_in(lptr, rb, rc2, (unsigned)(j + 1), lo, hi);
-        append_if_in(lptr, rc, rc2, (unsigned)(j + 2), lo, hi);
-        append_if_in(lptr, rd, rc2, (unsigned)(j + 3), lo, hi);
-        j += 4;
-    }
-#pragma unroll 1 // measured: no unroll 457, x2 468, x4 477 us (the remainder cascade runs at 9-11 lanes)
-    for (; j + 3 < hi; j += 4) {
-        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
-        append_if(lptr, ra, rc2, (unsigned)j);
-        append_if(lptr, rb, rc2, (unsigned)(j + 1));
-        append_if(lptr, rc, rc2, (unsigned)(j + 2));
-        append_if(lptr, rd, rc2, (unsigned)(j + 3));
-    }
-    if (j < hi) {
-        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
-        append_if(lptr, ra, rc2, (unsigned)j);
-        append_if_lt(lptr, rb, rc2, (unsigned)(j + 1), hi);
-        append_if_lt(lptr, rc, rc2, (unsigned)(j + 2), hi);
-        append_if_lt(lptr, rd, rc2, (unsigned)(j + 3), hi);
-    }
 }
 
 // Asynchronous copy (LDGSTS, no register round trip) of global particles [g0, g0 + len)
@@ -310,7 +245,7 @@ __device__ __forceinline__ void stage_copy(SM &S, const float4 *__restrict__ pos
 // Second pass over a staged range: periodic-image shift, SoA copy, id (| species << 30) into
 // the velocity word, zeroed accumulators.
 template <int KMODE, class SM>
-__device__ __forceinline__ void stage_fix(SM &S, int s0, int len, int g0, float sx, float sy, float sz, int lane)
+__device__ __forceinline__ void stage_fix(SM &S, int s0, int len, float sx, float sy, float sz, int lane)
 {
     for (int k = lane; k < len; k += 32) {
         const int s = s0 + k;
@@ -321,14 +256,9 @@ __device__ __forceinline__ void stage_fix(SM &S, int s0, int len, int g0, float 
         uint32_t word = __float_as_uint(p.w);
         if constexpr (KMODE == 3) word |= (uint32_t)__float_as_int(S.sv[s].w) << 30;
         S.sv[s].w = __uint_as_float(word);
-#if FT_GRED
-        S.gidx[s] = g0 + k;
-#else
-        (void)g0;
         S.acc[0][s] = 0;
         S.acc[1][s] = 0;
         S.acc[2][s] = 0;
-#endif
     }
 }
 
@@ -420,14 +350,10 @@ struct PairCursor {
 // Add (x, y, z) to staged particle s's force.
 __device__ __forceinline__ void acc_add(ForceTileSmem &S, float4 *frc, int s, AccT x, AccT y, AccT z)
 {
-#if FT_GRED
-    atomicAdd(&frc[S.gidx[s]], make_float4(x, y, z, 0.0f));
-#else
     (void)frc;
     atomicAdd(&S.acc[0][s], x); // native ATOMS.ADD (the fp32 variant is a CAS loop)
     atomicAdd(&S.acc[1][s], y);
     atomicAdd(&S.acc[2][s], z);
-#endif
 }
 
 __device__ __forceinline__ void cursor_load(PairCursor &c, const ForceTileSmem &S)
@@ -661,9 +587,9 @@ __device__ __forceinline__ void tile_stage_fix(SM &S, const TileTab &T, const Ti
         const int c0 = (sxa + FT_ROWPAD) * row;
         const int a0 = T.soff[c0], b0 = T.soff[c0 + 1], c0s = T.soff[c0 + bx + 1], e0 = T.rend[row];
         const int mlo = wrap_lo ? b0 : a0, mhi = wrap_hi ? c0s : e0;
-        if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, T.cgs[c0], -g.L[0], sy, sz, lane);
-        stage_fix<KMODE>(S, mlo, mhi - mlo, wrap_lo ? T.cgs[c0 + 1] : T.cgs[c0], 0.0f, sy, sz, lane);
-        if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, T.cgs[c0 + bx + 1], g.L[0], sy, sz, lane);
+        if (wrap_lo) stage_fix<KMODE>(S, a0, b0 - a0, -g.L[0], sy, sz, lane);
+        stage_fix<KMODE>(S, mlo, mhi - mlo, 0.0f, sy, sz, lane);
+        if (wrap_hi) stage_fix<KMODE>(S, c0s, e0 - c0s, g.L[0], sy, sz, lane);
         if (lane < FT_GAP) { // sentinels: a sweep block running past a row end fails the cutoff test
             S.sx[e0 + lane] = FT_FAR;
             S.sy[e0 + lane] = FT_FAR;
@@ -720,7 +646,6 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 #ifndef PROBE_NOSWEEP // timing probes: compile the sweep / pair walk out; wrong forces
 #define PROBE_NOSWEEP 0
 #endif
-#if FT_FUSED
             // Fused sweep.  The first aligned block of segment 0 (own cell after i, next cell)
             // is the only masked one (j > i) and is peeled: every lane runs exactly one.  All
             // later blocks are unmasked: a block running past a segment end meets a cell two
@@ -730,10 +655,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
             const int a0s = s_i + 1, b0s = T.soff[c + 2];
             const int j0 = a0s & ~3;
-#ifndef FT_SEG0LOCK
-#define FT_SEG0LOCK 0
-#endif
-            if (!FT_SEG0LOCK && !PROBE_NOSWEEP && j0 < b0s) {
+            if (!PROBE_NOSWEEP && j0 < b0s) {
                 float ra, rb, rc, rd;
                 r2_quad(S, j0, PX, PY, PZ, ra, rb, rc, rd);
                 append_if_in(lptr, ra, pp.rc2, (unsigned)j0, a0s, b0s);
@@ -757,7 +679,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 if (k == 0) {
                     a = j0 + 4;
                     b = b0s;
-                    ne = !FT_SEG0LOCK && a < b; // FT_SEG0LOCK: the own cell runs after the rows
+                    ne = a < b;
                 } else {
                     const int cs = (k == 1) ? c1 : c1 - 2 * rs + rowz + (k - 2) * rs;
                     const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
@@ -827,82 +749,6 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                     q4 = 0;
                 }
             }
-#if FT_SEG0LOCK
-            // own cell A and A + x after the rows: every lane of A sweeps A's whole range at the
-            // same iteration (shared-memory broadcast), keeping only j > i
-            if (!PROBE_NOSWEEP) {
-                j = T.soff[c] & ~3;
-                if (!full) {
-#pragma unroll 1
-                    for (; j < b0s; j += 4) {
-                        if ((int)(lptr - lbase) > 2 * (FT_LCAP - 4)) {
-                            full = true;
-                            break;
-                        }
-                        float ra, rb, rc, rd;
-                        r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
-                        append_if_gt(lptr, ra, pp.rc2, (unsigned)j, s_i);
-                        append_if_gt(lptr, rb, pp.rc2, (unsigned)(j + 1), s_i);
-                        append_if_gt(lptr, rc, pp.rc2, (unsigned)(j + 2), s_i);
-                        append_if_gt(lptr, rd, pp.rc2, (unsigned)(j + 3), s_i);
-                    }
-                }
-                if (full) {
-                    const float4 pi = ldp<KMODE>(S, s_i), vi = ldv<KMODE>(S, s_i);
-                    for (j = max(j, a0s); j < b0s; ++j) {
-                        if (!(r2_one(S, j, px, py, pz) < pp.rc2)) continue;
-                        float dx, dy, dz;
-                        const float s =
-                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, j), ldv<KMODE>(S, j), ks, rec, err, dx, dy, dz);
-                        const AccT qx = acc_q(dx, s), qy = acc_q(dy, s), qz = acc_q(dz, s);
-                        acc_add(S, frc, s_i, qx, qy, qz);
-                        acc_add(S, frc, j, -qx, -qy, -qz);
-                    }
-                }
-            }
-#endif
-#else
-#pragma unroll // all five segments (measured 457 -> 449 us against a rolled loop)
-            for (int k = 0; k < (PROBE_NOSWEEP ? 0 : 5); ++k) {
-                // segment k: 0 = own cell after i + next cell; 1 = y+1 row; 2..4 = z+1 rows (y-1..y+1)
-                const int cs = (k == 0) ? c : (k == 1 ? c1 : c1 - 2 * rs + rowz + (k - 2) * rs);
-                int a = (k == 0) ? s_i + 1 : T.soff[cs];
-                int b = T.soff[cs + (k == 0 ? 2 : 3)];
-                if (k > 0) {
-                    const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
-                    const float qz = (k == 1) ? 0.0f : dzr;
-                    const float q = qy * qy + qz * qz;
-                    if (!(q < pp.rc2)) continue;
-                    if (!(dxl * dxl + q < pp.rc2)) a = T.soff[cs + 1];
-                    if (!(dxr * dxr + q < pp.rc2)) b = T.soff[cs + 2];
-                }
-                // a chunk of m candidates adds at most m entries: sweep in chunks that fit the
-                // remaining list capacity; once the list is full (first particle of a crowded
-                // cell, ~4 sigma) the remaining candidates are evaluated in place
-                while (a < b) {
-                    const int room = FT_LCAP - (int)((lptr - lbase) >> 1);
-                    if (room <= 0) {
-                        full = true;
-                        break;
-                    }
-                    const int e = min(b, a + room);
-                    sweep(S, lptr, a, e, px, py, pz, pp.rc2);
-                    a = e;
-                }
-                if (full) {
-                    const float4 pi = ldp<KMODE>(S, s_i), vi = ldv<KMODE>(S, s_i);
-                    for (; a < b; ++a) {
-                        if (!(r2_one(S, a, px, py, pz) < pp.rc2)) continue;
-                        float dx, dy, dz;
-                        const float s =
-                            pair_eval<RECORD, KMODE>(pp, fx, pi, vi, ldp<KMODE>(S, a), ldv<KMODE>(S, a), ks, rec, err, dx, dy, dz);
-                        const AccT qx = acc_q(dx, s), qy = acc_q(dy, s), qz = acc_q(dz, s);
-                        acc_add(S, frc, s_i, qx, qy, qz);
-                        acc_add(S, frc, a, -qx, -qy, -qz);
-                    }
-                }
-            }
-#endif
             if (full) atomicAdd(&err[6], 1); // statistics: in-place evaluations
             cnt = (int)(lptr - lbase) >> 1;
         }
@@ -960,8 +806,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             }
 #pragma unroll
             for (int k = 0; k < FT_NCUR; ++k) cursor_flush(cu[k], S, frc);
-            // fixed point: one pair must stay below 2^21 units; fp32 (FT_GRED): only non-finite
-            if (FT_GRED ? !(amax <= 3.0e38f) : amax > fx.mag_lim * fx.scale)
+            if (amax > fx.mag_lim * fx.scale) // one pair must stay below 2^21 fixed-point units
                 raise_err(err, ERR_RANGE, (int)w_id<KMODE>(cu[0].vi.w));
         }
         __syncwarp(); // the lists and the owner table are rewritten by the next round
@@ -1036,7 +881,7 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     if (tile_overflows(T, G)) {
         if (tid == 0) atomicAdd(&err[T.total > FT_SCAP ? 4 : 5], 1); // fallback statistics
         tile_fallback<RECORD, KMODE>(pos, vel, frc, start, g, pp, fx, ks, rec, err, G.x0, G.y0, G.z0, G.bx, G.by,
-                                     G.bz, FT_GRED ? 1.0f : fx.inv_scale);
+                                     G.bz, fx.inv_scale);
         return;
     }
     tile_stage_issue(S, T, G, g, pos, vel, warp, lane);
@@ -1045,10 +890,8 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     tile_stage_fix<KMODE>(S, T, G, g, warp, lane);
     __syncthreads();
     tile_pairs<RECORD, KMODE>(S, T, G, g, pp, fx, ks, rec, err, frc, tid, warp, lane);
-#if !FT_GRED
     __syncthreads();
     tile_flush(S, T, G, g, fx, frc, warp, lane);
-#endif
 }
 
 } // namespace dpd
