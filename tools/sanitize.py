@@ -15,6 +15,14 @@ from paper_1911_04712_b200 import capi  # noqa: E402
 
 cfg = workloads.CONFIGS["parity"]
 pos, vel = workloads.make_config(cfg)
+# a ragged box at rho = 8: partial edge tiles (1-3 home cells wide), sweep blocks running into
+# the sentinel gaps after every staged row
+rg = workloads.Config("ragged", (11.3, 9.7, 7.2), 8.0, 25.0, 4.5, 1.0, 0.5, 0.005)
+rp, rv = workloads.make_config(rg)
+d = capi.DPD(rg.box, rg.rc, rg.a, rg.gamma, rg.kT, rg.power, rg.dt, rg.seed)
+d.set_particles(rp, rv)
+d.step(3)
+d.get_forces()
 for k in (0, 1):
     d = capi.DPD(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
     d.set_option("force_kernel", k)
