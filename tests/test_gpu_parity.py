@@ -524,14 +524,18 @@ def test_full_size_sampled_parity_other_configs(name):
 PAIRSET_BOXES = [(11.3, 9.7, 7.2), (17.0, 13.0, 6.0), (9.0, 6.0, 5.0), (8.0, 8.0, 8.0), (3.5, 17.0, 5.0)]
 
 
-@pytest.mark.parametrize("box", PAIRSET_BOXES)
-def test_tiled_pair_set_equals_reference_kernel(box):
+# (box, r_c, rho): r_c = 1 at rho = 8, and cells wider / narrower than one unit (h = L / floor(L / r_c))
+PAIRSET_CASES = [(b, 1.0, 8.0) for b in PAIRSET_BOXES] + [((12.0, 9.1, 8.0), 1.3, 3.0), ((7.9, 6.5, 10.0), 0.8, 8.0)]
+
+
+@pytest.mark.parametrize("box,rc,rho", PAIRSET_CASES)
+def test_tiled_pair_set_equals_reference_kernel(box, rc, rho):
     """The tiled kernel's fused sweep tests whole 4-candidate blocks past segment ends and relies
     on geometry (cells two apart are farther than r_c) and per-row sentinels to reject them.
     The pair set it evaluates must equal the reference thread-per-particle kernel's exactly on
     the same state (no duplicate, none missing), up to pairs inside the fp32 cutoff window,
-    over 40 steps of rho = 8."""
-    cfg = workloads.Config("pairset", box, 8.0, 25.0, 4.5, 1.0, 0.5, 0.005)
+    over 40 steps; no tile may take the global-memory fallback (the sweep itself is under test)."""
+    cfg = workloads.Config("pairset", box, rho, 25.0, 4.5, 1.0, 0.5, 0.005, rc=rc)
     pos0, vel0 = workloads.make_config(cfg)
     d = _ctx(cfg, kernel=0)
     d.set_particles(pos0, vel0)
@@ -559,3 +563,5 @@ def test_tiled_pair_set_equals_reference_kernel(box):
                     f"step {s}: {diff.size} pairs differ away from the cutoff (r2 = {r2[:5]})"
         if s < 40:
             d.step(1)
+    from paper_1911_04712_b200 import capi
+    assert capi.dpd_get_stat(d.ctx, "fallback_tiles") == 0
