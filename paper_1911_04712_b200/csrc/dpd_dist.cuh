@@ -267,17 +267,24 @@ __device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, 
 }
 
 // ---- row a9, warp per boundary cell ------------------------------------------------------
-// One warp per boundary cell of the list above: its local particles (<= 32 per pass, held
-// one per lane) against the ghosts of its halo neighbour cells, concatenated into one list
-// and taken 32 at a time (one ghost per lane, i broadcast by shuffle); in-cutoff combinations
-// are compacted into a per-warp queue and evaluated 32 at a time -- every lane busy in both
-// phases.  One-sided (C-19): the
-// i-side sums go to fixed-point shared accumulators, then once to frc.
+// One warp per boundary cell of the list above.  The ghosts of its halo neighbour cells are
+// staged once per chunk of kHcG into the warp's shared buffer -- shifted into the local frame,
+// velocity and id alongside -- with coalesced loads whose latencies overlap (round 1 gathered
+// them from global memory per candidate chunk and again per evaluated pair: the kernel was
+// bound by those load latencies).  Its local particles (<= 32 per pass, in shared memory for
+// broadcast reads) are tested against the staged ghosts one ghost per lane, kHcI locals per
+// round; in-cutoff combinations are compacted into a per-warp queue and evaluated 32 at a time
+// with both sides read from shared memory.  One-sided (C-19): the i-side sums go to
+// fixed-point shared accumulators, then once to frc.
 constexpr int kHcWarps = 4;
-constexpr int kHcI = 4; // local particles tested per candidate round
+constexpr int kHcI = 4;   // local particles tested per candidate round
+#ifndef KHC_G
+#define KHC_G 128
+#endif
+constexpr int kHcG = KHC_G; // ghosts staged per chunk (a face cell has ~72, an edge ~120 at rho = 8)
 
 template <int KMODE>
-__global__ void __launch_bounds__(32 * kHcWarps)
+__global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps per SM
     k_force_halo_cells(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
                        const int *__restrict__ bcells, const int *__restrict__ start,
                        const float4 *__restrict__ gpos, const float4 *__restrict__ gvel,
@@ -286,6 +293,9 @@ __global__ void __launch_bounds__(32 * kHcWarps)
 {
     __shared__ unsigned qbuf[kHcWarps][32 + 32 * kHcI]; // < 32 pending + kHcI x 32 new
     __shared__ float4 spi[kHcWarps][32];                // the cell's local positions (broadcast reads)
+    __shared__ float4 svi[kHcWarps][32];                // ... and velocities
+    __shared__ float4 sgp[kHcWarps][kHcG];              // staged ghosts: local-frame position, id bits
+    __shared__ float4 sgv[kHcWarps][kHcG];              // ... velocity, species
     __shared__ int acc[kHcWarps][3][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned *q = qbuf[warp];
@@ -325,87 +335,92 @@ __global__ void __launch_bounds__(32 * kHcWarps)
             }
             acc[warp][0][lane] = acc[warp][1][lane] = acc[warp][2][lane] = 0;
             spi[warp][lane] = pi;
-            __syncwarp();
-            int qn = 0;
-            // evaluate queue entries [0, cnt): lane k takes entry k
-            auto evaluate = [&](int cnt) {
-                const unsigned e = lane < cnt ? q[lane] : 0u;
-                const int j = (int)(e & 0x3FFFFFu), ii = (int)((e >> 22) & 31u), d = (int)(e >> 27);
-                const float ix = __shfl_sync(0xffffffffu, pi.x, ii), iy = __shfl_sync(0xffffffffu, pi.y, ii),
-                            iz = __shfl_sync(0xffffffffu, pi.z, ii), iw = __shfl_sync(0xffffffffu, pi.w, ii);
-                const float ux = __shfl_sync(0xffffffffu, vi.x, ii), uy = __shfl_sync(0xffffffffu, vi.y, ii),
-                            uz = __shfl_sync(0xffffffffu, vi.z, ii), uw = __shfl_sync(0xffffffffu, vi.w, ii);
-                const float shx = __shfl_sync(0xffffffffu, hsh[0], d), shy = __shfl_sync(0xffffffffu, hsh[1], d),
-                            shz = __shfl_sync(0xffffffffu, hsh[2], d);
-                if (lane < cnt) {
-                    const float4 pj = gpos[j], vj = gvel[j];
-                    const float rx = ix - (pj.x + shx), ry = iy - (pj.y + shy), rz = iz - (pj.z + shz);
-                    const float r2 = rx * rx + ry * ry + rz * rz;
-                    const float dv = rx * (ux - vj.x) + ry * (uy - vj.y) + rz * (uz - vj.z);
-                    float mag;
-                    const float sc = pair_mag<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(iw),
-                                                     (uint32_t)__float_as_int(pj.w), ks, __float_as_int(uw),
-                                                     __float_as_int(vj.w), mag);
-                    amax = fmaxf(amax, fabsf(mag));
-                    atomicAdd(&acc[warp][0][ii], __float_as_int(__fmaf_rn(sc * rx, scale, 12582912.0f)) - 0x4B400000);
-                    atomicAdd(&acc[warp][1][ii], __float_as_int(__fmaf_rn(sc * ry, scale, 12582912.0f)) - 0x4B400000);
-                    atomicAdd(&acc[warp][2][ii], __float_as_int(__fmaf_rn(sc * rz, scale, 12582912.0f)) - 0x4B400000);
-                }
-            };
-            // the ghosts of all halo neighbour cells as one list, 32 per chunk with one ghost
-            // per lane (position shifted to the local frame once), tested against the cell's
-            // local particles one at a time (i broadcast by shuffle): the chunk's candidates
-            // cost a few instructions per lane-pair, no per-candidate index math or gather
-            for (int cb = 0; cb < G; cb += 32) {
-                const int gi = cb + lane;
-                int d = 0; // largest halo lane with prefix <= gi (the prefix is non-decreasing)
+            svi[warp][lane] = vi;
+            for (int gb = 0; gb < G; gb += kHcG) {
+                const int gn = min(kHcG, G - gb);
+                __syncwarp(); // the previous chunk's evaluations are done with the buffer
+                // stage ghosts [gb, gb + gn): halo cell of each by a search over the prefix
+                for (int k = lane; k < ((gn + 31) & ~31); k += 32) {
+                    const int gi = gb + k;
+                    int d = 0; // largest halo lane with prefix <= gi (the prefix is non-decreasing)
 #pragma unroll
-                for (int stp = 16; stp > 0; stp >>= 1) {
-                    const int t = d + stp;
-                    const int off_t = __shfl_sync(0xffffffffu, hex, t & 31);
-                    if (t < 27 && off_t <= gi) d = t;
+                    for (int stp = 16; stp > 0; stp >>= 1) {
+                        const int t = d + stp;
+                        const int off_t = __shfl_sync(0xffffffffu, hex, t & 31);
+                        if (t < 27 && off_t <= gi) d = t;
+                    }
+                    const int a = __shfl_sync(0xffffffffu, ha, d), off = __shfl_sync(0xffffffffu, hex, d);
+                    const float shx = __shfl_sync(0xffffffffu, hsh[0], d), shy = __shfl_sync(0xffffffffu, hsh[1], d),
+                                shz = __shfl_sync(0xffffffffu, hsh[2], d);
+                    if (k < gn) {
+                        const int jidx = a + gi - off;
+                        const float4 pj = gpos[jidx];
+                        sgp[warp][k] = make_float4(pj.x + shx, pj.y + shy, pj.z + shz, pj.w);
+                        sgv[warp][k] = gvel[jidx];
+                    }
                 }
-                const int a = __shfl_sync(0xffffffffu, ha, d), off = __shfl_sync(0xffffffffu, hex, d);
-                const float shx = __shfl_sync(0xffffffffu, hsh[0], d), shy = __shfl_sync(0xffffffffu, hsh[1], d),
-                            shz = __shfl_sync(0xffffffffu, hsh[2], d);
-                const bool gv = gi < G;
-                const unsigned jidx = gv ? (unsigned)(a + gi - off) : 0u;
-                float px = 3.0e30f, py = 0.0f, pz = 0.0f; // invalid lane: never within r_c
-                if (gv) {
-                    const float4 pj = gpos[jidx];
-                    px = pj.x + shx;
-                    py = pj.y + shy;
-                    pz = pj.z + shz;
-                }
-                const unsigned tag = jidx | ((unsigned)d << 27);
-                for (int ii = 0; ii < ni; ii += kHcI) { // kHcI local particles per round
-                    unsigned m[kHcI];
-                    bool h[kHcI];
-#pragma unroll
-                    for (int u = 0; u < kHcI; ++u) {
-                        const float4 p = spi[warp][min(ii + u, 31)]; // LDS.128 broadcast
-                        const float rx = p.x - px, ry = p.y - py, rz = p.z - pz;
+                __syncwarp();
+                int qn = 0;
+                // evaluate queue entries [0, cnt): lane k takes entry k (both sides from shared memory)
+                auto evaluate = [&](int cnt) {
+                    if (lane < cnt) {
+                        const unsigned e = q[lane];
+                        const int k = (int)(e & 0xFFFFu), ii = (int)(e >> 16);
+                        const float4 pj = sgp[warp][k], vj = sgv[warp][k];
+                        const float4 p = spi[warp][ii], u = svi[warp][ii];
+                        const float rx = p.x - pj.x, ry = p.y - pj.y, rz = p.z - pj.z;
                         const float r2 = rx * rx + ry * ry + rz * rz;
-                        h[u] = ii + u < ni && r2 < pp.rc2 && r2 > 0.0f;
-                        m[u] = __ballot_sync(0xffffffffu, h[u]);
+                        const float dv = rx * (u.x - vj.x) + ry * (u.y - vj.y) + rz * (u.z - vj.z);
+                        float mag;
+                        const float sc = pair_mag<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(p.w),
+                                                         (uint32_t)__float_as_int(pj.w), ks, __float_as_int(u.w),
+                                                         __float_as_int(vj.w), mag);
+                        amax = fmaxf(amax, fabsf(mag));
+                        atomicAdd(&acc[warp][0][ii], __float_as_int(__fmaf_rn(sc * rx, scale, 12582912.0f)) - 0x4B400000);
+                        atomicAdd(&acc[warp][1][ii], __float_as_int(__fmaf_rn(sc * ry, scale, 12582912.0f)) - 0x4B400000);
+                        atomicAdd(&acc[warp][2][ii], __float_as_int(__fmaf_rn(sc * rz, scale, 12582912.0f)) - 0x4B400000);
                     }
-                    const unsigned lt = lanemask_lt();
+                };
+                // the staged ghosts, 32 per chunk with one ghost per lane, tested against the
+                // cell's local particles kHcI at a time (broadcast LDS.128)
+                for (int cb = 0; cb < gn; cb += 32) {
+                    const int k = cb + lane;
+                    float px = 3.0e30f, py = 0.0f, pz = 0.0f; // beyond the chunk: never within r_c
+                    if (k < gn) {
+                        const float4 pj = sgp[warp][k];
+                        px = pj.x;
+                        py = pj.y;
+                        pz = pj.z;
+                    }
+                    for (int ii = 0; ii < ni; ii += kHcI) { // kHcI local particles per round
+                        unsigned m[kHcI];
+                        bool h[kHcI];
 #pragma unroll
-                    for (int u = 0; u < kHcI; ++u) {
-                        if (h[u]) q[qn + __popc(m[u] & lt)] = tag | ((unsigned)(ii + u) << 22);
-                        qn += __popc(m[u]);
-                    }
-                    __syncwarp();
-                    while (qn >= 32) {
-                        evaluate(32);
+                        for (int u = 0; u < kHcI; ++u) {
+                            const float4 p = spi[warp][min(ii + u, 31)]; // LDS.128 broadcast
+                            const float rx = p.x - px, ry = p.y - py, rz = p.z - pz;
+                            const float r2 = rx * rx + ry * ry + rz * rz;
+                            h[u] = ii + u < ni && r2 < pp.rc2 && r2 > 0.0f;
+                            m[u] = __ballot_sync(0xffffffffu, h[u]);
+                        }
+                        const unsigned lt = lanemask_lt();
+#pragma unroll
+                        for (int u = 0; u < kHcI; ++u) {
+                            if (h[u]) q[qn + __popc(m[u] & lt)] = (unsigned)k | ((unsigned)(ii + u) << 16);
+                            qn += __popc(m[u]);
+                        }
                         __syncwarp();
-                        for (int k = lane; k < qn - 32; k += 32) q[k] = q[k + 32];
-                        qn -= 32;
-                        __syncwarp();
+                        while (qn >= 32) {
+                            evaluate(32);
+                            __syncwarp();
+                            for (int t = lane; t < qn - 32; t += 32) q[t] = q[t + 32];
+                            qn -= 32;
+                            __syncwarp();
+                        }
                     }
                 }
+                if (qn > 0) evaluate(qn);
             }
-            if (qn > 0) evaluate(qn);
             __syncwarp();
             if (lane < ni) {
                 float4 f = frc[s0 + ib + lane];
