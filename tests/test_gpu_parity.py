@@ -565,3 +565,22 @@ def test_tiled_pair_set_equals_reference_kernel(box, rc, rho):
             d.step(1)
     from paper_1911_04712_b200 import capi
     assert capi.dpd_get_stat(d.ctx, "fallback_tiles") == 0
+
+
+def test_kernel_switch_keeps_force_buffers_consistent():
+    """The sort's target force buffer is zeroed a step ahead: by the tiled kernel's first wave,
+    or by a memset when the reference kernel computes the step.  Alternating the two kernels
+    step by step must keep every step's forces at the oracle's (config 1, C-13 protocol)."""
+    cfg = workloads.CONFIGS["parity"]
+    p = _params(cfg)
+    eps, eps_img = windows(cfg.box)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg, kernel=0)
+    d.set_particles(pos0, vel0)
+    for s in range(9):
+        pos, u, F, ids = d.get_state()
+        x_id, u_id, F_id = by_id(ids, pos, u, F)
+        F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, eps=eps, eps_image=eps_img)
+        check_forces(F_id, F_ref, allow)
+        d.set_option("force_kernel", (s + 1) % 2)
+        d.step(1)
