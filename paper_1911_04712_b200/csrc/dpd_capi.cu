@@ -387,9 +387,14 @@ int phase_bin(dpd_ctx *c, const IntegP &ip, bool with_mig = true)
     if (with_mig) {
         TRY(launch(c, KID_MIGRATE, [&] { k_zero_headers<<<1, 32, 0, c->stream>>>(mig); }));
     }
+    const bool lean = !c->dist && ip.nwall == 0 && ip.frozen_mask == 0;
     return launch(c, KID_BIN, [&] {
-        k_bin<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p, count_ptr(c), g, ip,
-                                                         c->count.p, c->rank_buf.p, mig, c->err.p);
+        if (lean)
+            k_bin<true><<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p, count_ptr(c),
+                                                                    g, ip, c->count.p, c->rank_buf.p, mig, c->err.p);
+        else
+            k_bin<false><<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p, count_ptr(c),
+                                                                     g, ip, c->count.p, c->rank_buf.p, mig, c->err.p);
     });
 }
 
@@ -416,11 +421,16 @@ int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true, bool zero_tar
         k_scan<<<ntile, kScanThreads, 0, c->stream>>>(c->count.p, c->start[sd].p, g.ncell, c->scan_state.p,
                                                       c->scan_epoch.p);
     }));
+    const bool lean = !c->dist && ip.nwall == 0 && ip.frozen_mask == 0; // as phase_bin: identical advance
     TRY(launch(c, KID_SCATTER, [&] {
-        k_scatter<<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(c->pos[s].p, c->vel[s].p, c->frc[s].p,
-                                                              c->start[ss].p + g.ncell, g, ip, c->start[sd].p,
-                                                              c->rank_buf.p, c->pos[d].p, c->vel[d].p, (int)c->n_cap,
-                                                              c->err.p);
+        if (lean)
+            k_scatter<true><<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(
+                c->pos[s].p, c->vel[s].p, c->frc[s].p, c->start[ss].p + g.ncell, g, ip, c->start[sd].p, c->rank_buf.p,
+                c->pos[d].p, c->vel[d].p, (int)c->n_cap, c->err.p);
+        else
+            k_scatter<false><<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(
+                c->pos[s].p, c->vel[s].p, c->frc[s].p, c->start[ss].p + g.ncell, g, ip, c->start[sd].p, c->rank_buf.p,
+                c->pos[d].p, c->vel[d].p, (int)c->n_cap, c->err.p);
     }));
     if (with_mig) {
         const dim3 grid(nblk(c->mig.maxcap, 256), 27);

@@ -88,10 +88,12 @@ __device__ __forceinline__ float wall_sdf(const IntegP &ip, float x, float y, fl
 // (32 halvings) finds the last point x + t u with s <= 0, the particle is placed there and
 // u' <- 2 u_w - u'.  Frozen species do not move.  Explicit _rn intrinsics pin the rounding
 // so k_bin and k_scatter agree bit-for-bit.
+template <bool LEAN>
 __device__ __forceinline__ void advance(const Geom &g, const IntegP &ip, const float4 p, const float4 v,
                                         const float4 f, float3 &xn, float3 &un)
 {
-    if (ip.frozen_mask && is_frozen(ip, v)) {
+    // LEAN: no frozen species, no walls (k_bin / k_scatter instantiate both forms identically)
+    if (!LEAN && ip.frozen_mask && is_frozen(ip, v)) {
         un = make_float3(v.x, v.y, v.z);
         xn = make_float3(p.x, p.y, p.z);
         return;
@@ -103,7 +105,7 @@ __device__ __forceinline__ void advance(const Geom &g, const IntegP &ip, const f
     xn.x = __fmaf_rn(ip.dt, un.x, p.x);
     xn.y = __fmaf_rn(ip.dt, un.y, p.y);
     xn.z = __fmaf_rn(ip.dt, un.z, p.z);
-    if (ip.nwall > 0) {
+    if (!LEAN && ip.nwall > 0) {
         int arg;
         if (wall_sdf(ip, xn.x, xn.y, xn.z, arg) > 0.0f) {
             float lo = 0.0f, hi = ip.dt;
@@ -261,6 +263,7 @@ __device__ __forceinline__ int dir_index(int dx, int dy, int dz) { return (dx + 
 // ---------------------------------------------------------------------------------------
 // 8 resident blocks (full occupancy, 32 registers) hide the load + histogram-atomic latency:
 // measured 29.1 -> 27.0 us at 2.1 M particles
+template <bool LEAN> // LEAN: single domain, no walls, no frozen species (the bench / eq64 path)
 __global__ void __launch_bounds__(256, 8) k_bin(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                              const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
                                              IntegP ip, int *__restrict__ count, int *__restrict__ rank, Msgs mig,
@@ -279,11 +282,11 @@ __global__ void __launch_bounds__(256, 8) k_bin(const float4 *__restrict__ pos, 
     if (i < n) {
         const float4 p = pos[i], v = vel[i], f = frc[i];
         float3 xn, un;
-        advance(g, ip, p, v, f, xn, un);
+        advance<LEAN>(g, ip, p, v, f, xn, un);
         int dx = 0, dy = 0, dz = 0;
-        if (g.split[0]) dx = xn.x < 0.0f ? -1 : (xn.x >= g.L[0] ? 1 : 0);
-        if (g.split[1]) dy = xn.y < 0.0f ? -1 : (xn.y >= g.L[1] ? 1 : 0);
-        if (g.split[2]) dz = xn.z < 0.0f ? -1 : (xn.z >= g.L[2] ? 1 : 0);
+        if (!LEAN && g.split[0]) dx = xn.x < 0.0f ? -1 : (xn.x >= g.L[0] ? 1 : 0);
+        if (!LEAN && g.split[1]) dy = xn.y < 0.0f ? -1 : (xn.y >= g.L[1] ? 1 : 0);
+        if (!LEAN && g.split[2]) dz = xn.z < 0.0f ? -1 : (xn.z >= g.L[2] ? 1 : 0);
         if (dx | dy | dz) {
             // migrant: into the destination frame.  x - (-L) = x + L can round up to L for
             // x within an ulp below 0; keep it inside [0, L) (the C-10 rule for wrapped axes)
@@ -454,6 +457,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, 
 // a4: scatter into cell order; recomputes a1 in registers (bit-identical to k_bin).  The
 // sorted force array it pairs with is already zero (k_force_tile zeroes it one step ahead).
 // ---------------------------------------------------------------------------------------
+template <bool LEAN>
 __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos, const float4 *__restrict__ vel,
                                                  const float4 *__restrict__ frc, const int *__restrict__ n_ptr, Geom g,
                                                  IntegP ip, const int *__restrict__ start,
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos,
     if (i >= *n_ptr || rank[i] < 0) return; // rank < 0: migrant, sent away
     const float4 p = pos[i], v = vel[i], f = frc[i];
     float3 xn, un;
-    advance(g, ip, p, v, f, xn, un);
+    advance<LEAN>(g, ip, p, v, f, xn, un);
     if (!finite3(xn.x, xn.y, xn.z) || !finite3(un.x, un.y, un.z) || !in_local_box(g, xn))
         xn = make_float3(0.0f, 0.0f, 0.0f);
     const int c = cell_index(g, xn.x, xn.y, xn.z);
