@@ -51,7 +51,7 @@ constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16
 constexpr int FT_LCAP = 40;                   // hits per home particle (mean 16.8, sd 4.1)
 constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 21 words per list (odd): conflict-free appends
 #ifndef FT_NCUR_DEF
-#define FT_NCUR_DEF 2
+#define FT_NCUR_DEF 1
 #endif
 constexpr int FT_NCUR = FT_NCUR_DEF;          // independent pair chains per lane (ILP)
 #ifndef FT_MINB
