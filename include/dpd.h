@@ -255,6 +255,19 @@ int dpd_create_dist(const double box[3], double rc, double a, double gamma, doub
                     double power, double dt, uint64_t seed, int rank, int world,
                     const int32_t grid[3], const uint8_t nccl_id[128], dpd_ctx **out);
 
+/* Create a one-rank NCCL context whose dimensions with split[k] != 0 are decomposed into
+ * one subdomain that is its own neighbour: the periodic halo and the leavers of those
+ * dimensions are packed into the 26-direction messages, sent with ncclSend / ncclRecv to the
+ * rank itself (a self-peer; NCCL matches them in posting order, increasing d) and received
+ * as ghosts / migrants -- P:234-247's exchange, P:243-247's overlap of the transfer with the
+ * local forces, run end to end on one GPU.  Results equal those of dpd_create's periodic
+ * context up to fp32 summation order.  nccl_id: a fresh id from dpd_nccl_unique_id.
+ * Errors: DPD_ERR_ARG (no split dimension, null pointers), DPD_ERR_CONFIG (< 3 cells per
+ * dimension), DPD_ERR_COMM (library built without NCCL, communicator init failed). */
+int dpd_create_loopback(const double box[3], double rc, double a, double gamma, double kT,
+                        double power, double dt, uint64_t seed, const int32_t split[3],
+                        const uint8_t nccl_id[128], dpd_ctx **out);
+
 /* Create an in-process group of prod(grid) subdomain contexts on the current device that
  * exchange ghosts / migrants by device copies instead of NCCL (same kernels, transport
  * swapped; used to test the decomposition on one GPU).  out receives grid-many contexts

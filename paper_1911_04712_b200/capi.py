@@ -63,6 +63,8 @@ SIGNATURES = [
     ("dpd_nccl_unique_id", C.c_int, [_vp]),
     ("dpd_create_dist", C.c_int, [_P(C.c_double), C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_uint64, C.c_int, C.c_int, _P(C.c_int32), _vp, _P(_vp)]),
+    ("dpd_create_loopback", C.c_int, [_P(C.c_double), C.c_double, C.c_double, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, C.c_uint64, _P(C.c_int32), _vp, _P(_vp)]),
     ("dpd_create_group", C.c_int, [_P(C.c_double), C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                    C.c_double, C.c_uint64, _P(C.c_int32), _P(_vp)]),
     ("dpd_group_step", C.c_int, [_P(_vp), C.c_int, C.c_int64]),
@@ -505,6 +507,18 @@ def dpd_create_dist(box, rc, a, gamma, kT, power, dt, seed, rank, world, grid, n
                              C.byref(out))
     if code != DPD_OK:
         raise DPDError(code, "dpd_create_dist failed (see stderr)")
+    return out
+
+
+def dpd_create_loopback(box, rc, a, gamma, kT, power, dt, seed, split, nccl_id=None):
+    L = load()
+    b = (C.c_double * 3)(*[float(x) for x in box])
+    sp = (C.c_int32 * 3)(*[int(x) for x in split])
+    uid = np.ascontiguousarray(dpd_nccl_unique_id() if nccl_id is None else nccl_id, np.uint8)
+    out = C.c_void_p()
+    code = L.dpd_create_loopback(b, rc, a, gamma, kT, power, dt, int(seed), sp, _ptr(uid), C.byref(out))
+    if code != DPD_OK:
+        raise DPDError(code, "dpd_create_loopback failed (see stderr)")
     return out
 
 

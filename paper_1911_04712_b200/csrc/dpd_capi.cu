@@ -56,10 +56,11 @@ enum KernelId {
     KID_GHOST_PACK,
     KID_GHOST_SORT,
     KID_HALO,
+    KID_NCCL, // NCCL send/recv groups (timed, not counted as this library's launches)
     KID_COUNT
 };
 const char *kKernelNames[KID_COUNT] = {"pack",    "bin",        "scan",       "scatter", "force", "gather",
-                                       "debug",   "migrate",    "ghost_pack", "ghost_sort", "halo"};
+                                       "debug",   "migrate",    "ghost_pack", "ghost_sort", "halo", "nccl"};
 
 template <class T>
 struct DevBuf {
@@ -627,6 +628,12 @@ int phase_halo(dpd_ctx *c, int64_t step)
 int exchange_nccl(dpd_ctx *c, MsgArea &m, cudaStream_t st)
 {
 #ifdef DPD_HAVE_NCCL
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (c->timing) {
+        ea = get_event(c);
+        eb = get_event(c);
+        cudaEventRecord(ea, st);
+    }
     NCCL_TRY(c, ncclGroupStart());
     for (int d = 0; d < 27; ++d) {
         if (m.bytes[d] == 0) continue;
@@ -634,6 +641,10 @@ int exchange_nccl(dpd_ctx *c, MsgArea &m, cudaStream_t st)
         NCCL_TRY(c, ncclRecv(m.recv.p + m.mr.off[d], m.bytes[d], ncclChar, c->peer_from[d], c->nccl, st));
     }
     NCCL_TRY(c, ncclGroupEnd());
+    if (c->timing) {
+        cudaEventRecord(eb, st);
+        c->pending.push_back({ea, eb, KID_NCCL});
+    }
     return DPD_OK;
 #else
     (void)m;
@@ -1253,8 +1264,11 @@ void setup_ranks(dpd_ctx *c, int rank, const int32_t grid[3])
     for (int k = 0; k < 3; ++k) c->origin[k] = (float)(c->coord[k] * c->sub[k]);
 }
 
+// loop[k] (may be null): dimension k is split although grid[k] == 1 -- its periodic halo and
+// migrants travel through the exchange to the rank itself (dpd_create_loopback).
 int create_common(const double box[3], double rc, double a, double gamma, double kT, double power, double dt,
-                  uint64_t seed, int rank, const int32_t grid[3], dpd_ctx **out, dpd_ctx *c)
+                  uint64_t seed, int rank, const int32_t grid[3], dpd_ctx **out, dpd_ctx *c,
+                  const int32_t *loop = nullptr)
 {
     int r = init_ctx(c, box, rc, a, gamma, kT, power, dt, seed);
     if (r != DPD_OK) return r;
@@ -1263,7 +1277,7 @@ int create_common(const double box[3], double rc, double a, double gamma, double
     for (int k = 0; k < 3; ++k) {
         if (grid[k] < 1) return fail(c, DPD_ERR_CONFIG, "grid[%d] = %d must be >= 1", k, grid[k]);
         sub[k] = box[k] / grid[k];
-        split[k] = grid[k] > 1;
+        split[k] = grid[k] > 1 || (loop && loop[k] != 0);
     }
     c->dist = split[0] || split[1] || split[2];
     TRY(setup_geometry(c, sub, split));
@@ -2018,6 +2032,33 @@ int dpd_create_dist(const double box[3], double rc, double a, double gamma, doub
 #endif
     if (r != DPD_OK) {
         fprintf(stderr, "dpd_create_dist: %s\n", c->last_error.c_str());
+        *out = nullptr;
+        dpd_destroy(c);
+    }
+    return r;
+}
+
+int dpd_create_loopback(const double box[3], double rc, double a, double gamma, double kT, double power, double dt,
+                        uint64_t seed, const int32_t split[3], const uint8_t nccl_id[128], dpd_ctx **out)
+{
+    if (!out || !box || !split || !nccl_id) return DPD_ERR_ARG;
+    *out = nullptr;
+    if (!(split[0] || split[1] || split[2])) return DPD_ERR_ARG;
+    dpd_ctx *c = new dpd_ctx();
+    const int32_t grid[3] = {1, 1, 1};
+    int r = create_common(box, rc, a, gamma, kT, power, dt, seed, 0, grid, out, c, split);
+#ifdef DPD_HAVE_NCCL
+    if (r == DPD_OK) {
+        ncclUniqueId u;
+        memcpy(&u, nccl_id, 128);
+        ncclResult_t nr = ncclCommInitRank(&c->nccl, 1, u, 0);
+        if (nr != ncclSuccess) r = fail(c, DPD_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+    }
+#else
+    if (r == DPD_OK) r = fail(c, DPD_ERR_COMM, "libdpd was built without NCCL");
+#endif
+    if (r != DPD_OK) {
+        fprintf(stderr, "dpd_create_loopback: %s\n", c->last_error.c_str());
         *out = nullptr;
         dpd_destroy(c);
     }

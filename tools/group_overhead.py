@@ -5,8 +5,12 @@ Times dpd_step / dpd_group_step with CUDA events after warm-up; prints one JSON 
 mode serial: every phase of every member on one stream (device copies of the packed
 counts); mode graph: the production task graph per member (ghost pack / exchange / sort on
 the communication streams, concurrent with the interior forces) with the capacity-padded
-messages the NCCL path sends (option group_task_graph).
-usage: python tools/group_overhead.py [L=128] [grid=2,2,2] [steps=50] [mode=graph]"""
+messages the NCCL path sends (option group_task_graph); mode loopback: ONE subdomain of
+the whole box whose dimensions with grid[k] = 1 in "split" are their own neighbour
+(dpd_create_loopback): the production task graph with the real NCCL send/recv (to the rank
+itself) -- at L = 128 and split 1,1,1 this is the per-GPU step of the weak-scaling series
+(128^3 per GPU, six exchanged faces) with the transfer through NCCL's self path.
+usage: python tools/group_overhead.py [L=128] [grid=2,2,2] [steps=50] [mode=graph|serial|loopback]"""
 import json
 import os
 import sys
@@ -43,6 +47,18 @@ d.set_particles(pos, vel)
 d.step(10)
 t_single = timed(d.step, steps)
 del d
+if mode == "loopback":
+    c = capi.dpd_create_loopback(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed, grid)
+    capi.dpd_set_particles_ex(c, pos, vel, np.arange(n, dtype=np.int32), 0)
+    capi.dpd_step(c, 10)
+    t_loop = timed(lambda k: capi.dpd_step(c, k), steps)
+    cnt = capi.dpd_get_count(c)
+    sched = [f"{slot}:{name}" for slot, name, _ in capi.dpd_step_schedule(c)]
+    capi.dpd_destroy(c)
+    print(json.dumps({"box": L, "n": n, "split": grid, "steps": steps, "mode": mode, "ms_per_step_single": t_single,
+                      "ms_per_step_loopback": t_loop, "overhead": t_loop / t_single - 1.0,
+                      "particles_conserved": int(cnt) == n, "schedule": sched}))
+    sys.exit(0)
 ctxs = capi.dpd_create_group(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed, grid)
 capi.dpd_set_option(ctxs[0], "group_task_graph", 1 if mode == "graph" else 0)
 ids = np.arange(n, dtype=np.int32)
