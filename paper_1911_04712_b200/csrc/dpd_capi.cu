@@ -1284,7 +1284,12 @@ int create_common(const double box[3], double rc, double a, double gamma, double
     setup_ranks(c, rank, grid);
     TRY(alloc_grid(c));
     if (c->dist) {
-        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+        // the communication stream at the highest priority: its ghost pack / exchange / sort
+        // become ready when the interior force kernel already fills every SM, and take the
+        // slots its CTAs free first, instead of queueing behind the whole force pass
+        int prio_lo = 0, prio_hi = 0;
+        CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CUDA_TRY(c, cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio_hi));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
         CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ghost, cudaEventDisableTiming));
     }
