@@ -184,7 +184,6 @@ struct dpd_ctx {
     int scur = 0; // which start array describes them (start[scur][ncell] = count)
     DevBuf<float4> pos[2], vel[2], frc[2];
     DevBuf<int> rank_buf, count, start[2];
-    DevBuf<int> sstart; // sub-bin starts of the current sort (kSubX per cell; count: sub-bin counts)
     DevBuf<unsigned long long> scan_state;
     DevBuf<unsigned> scan_epoch;
     DevBuf<int> err;
@@ -418,30 +417,27 @@ int phase_sort(dpd_ctx *c, const IntegP &ip, bool with_mig = true, bool zero_tar
             k_bin_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->count.p, c->rank_in.p, c->err.p);
         }));
     }
-    // sub-bin scan: sstart (kSubX per cell, the scatter's targets and the force sweep's row
-    // windows) and the cell starts start[sd] (every other consumer) in one pass
-    const int nsub = kSubX * g.ncell;
-    const int ntile = (nsub + kScanTile - 1) / kScanTile;
+    const int ntile = (g.ncell + kScanTile - 1) / kScanTile;
     TRY(launch(c, KID_SCAN, [&] {
-        k_scan<kSubX><<<ntile, kScanThreads, 0, c->stream>>>(c->count.p, c->sstart.p, nsub, c->scan_state.p,
-                                                             c->scan_epoch.p, c->start[sd].p);
+        k_scan<<<ntile, kScanThreads, 0, c->stream>>>(c->count.p, c->start[sd].p, g.ncell, c->scan_state.p,
+                                                      c->scan_epoch.p);
     }));
     const bool lean = !c->dist && ip.nwall == 0 && ip.frozen_mask == 0; // as phase_bin: identical advance
     TRY(launch(c, KID_SCATTER, [&] {
         if (lean)
             k_scatter<true><<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(
-                c->pos[s].p, c->vel[s].p, c->frc[s].p, c->start[ss].p + g.ncell, g, ip, c->sstart.p, c->rank_buf.p,
+                c->pos[s].p, c->vel[s].p, c->frc[s].p, c->start[ss].p + g.ncell, g, ip, c->start[sd].p, c->rank_buf.p,
                 c->pos[d].p, c->vel[d].p, (int)c->n_cap, c->err.p);
         else
             k_scatter<false><<<nblk(c->n_cap, 256), 256, 0, c->stream>>>(
-                c->pos[s].p, c->vel[s].p, c->frc[s].p, c->start[ss].p + g.ncell, g, ip, c->sstart.p, c->rank_buf.p,
+                c->pos[s].p, c->vel[s].p, c->frc[s].p, c->start[ss].p + g.ncell, g, ip, c->start[sd].p, c->rank_buf.p,
                 c->pos[d].p, c->vel[d].p, (int)c->n_cap, c->err.p);
     }));
     if (with_mig) {
         const dim3 grid(nblk(c->mig.maxcap, 256), 27);
         const Msgs mr = c->mig.mr;
         TRY(launch(c, KID_MIGRATE, [&] {
-            k_scatter_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->sstart.p, c->rank_in.p,
+            k_scatter_recv<<<grid, 256, 0, c->stream>>>(mr, g, c->mig.maxcap, c->start[sd].p, c->rank_in.p,
                                                         c->pos[d].p, c->vel[d].p, (int)c->n_cap, c->err.p);
         }));
     }
@@ -516,8 +512,8 @@ int force_pass(dpd_ctx *c, int64_t step, float4 *frc_out, PairRec rec, bool reco
         const int *st = c->start[c->scur].p;
         return launch(c, record ? KID_DEBUG : KID_FORCE, [&] {
 #define DPD_TILE(R, K)                                                                                              \
-    k_force_tile<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, c->sstart.p, g, pp, \
-                                                            fx, rk, rec, c->err.p, fzero, nzero)
+    k_force_tile<R, K><<<tgrid, FT_NTHR, smem, c->stream>>>(c->pos[b].p, c->vel[b].p, frc_out, st, g, pp, fx, rk, rec, \
+                                                            c->err.p, fzero, nzero)
             if (record) {
                 switch (c->kmode) {
                 case 0: DPD_TILE(true, 0); break;
@@ -578,7 +574,7 @@ int phase_ghost_sort(dpd_ctx *c, cudaStream_t st)
     TRY(launch(
         c, KID_GHOST_SORT,
         [&] {
-            k_scan<1><<<ntile, kScanThreads, 0, st>>>(c->gcount.p, c->gstart.p, g.ncell, c->gscan_state.p,
+            k_scan<<<ntile, kScanThreads, 0, st>>>(c->gcount.p, c->gstart.p, g.ncell, c->gscan_state.p,
                                                    c->scan_epoch.p + 1);
         },
         st));
@@ -1140,7 +1136,7 @@ int setup_geometry(dpd_ctx *c, const double len[3], const int split[3])
         ncell *= g.ext[k];
         c->sub[k] = len[k];
     }
-    if (ncell * kSubX > (int64_t)1 << 30) return fail(c, DPD_ERR_CONFIG, "too many cells (%lld)", (long long)ncell);
+    if (ncell > (int64_t)1 << 30) return fail(c, DPD_ERR_CONFIG, "too many cells (%lld)", (long long)ncell);
     g.ncell = (int)ncell;
     c->geom = g;
     return DPD_OK;
@@ -1226,17 +1222,13 @@ int init_ctx(dpd_ctx *c, const double box[3], double rc, double a, double gamma,
 int alloc_grid(dpd_ctx *c)
 {
     const int ncell = c->geom.ncell;
-    const size_t nsub = (size_t)kSubX * ncell;
-    CUDA_TRY(c, c->count.reserve(nsub + 16));
-    CUDA_TRY(c, c->sstart.reserve(nsub + 16));
-    CUDA_TRY(c, cudaMemset(c->sstart.p, 0, sizeof(int) * c->sstart.cap));
+    CUDA_TRY(c, c->count.reserve((size_t)ncell + 16));
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(c, c->start[b].reserve((size_t)ncell + 16));
         CUDA_TRY(c, cudaMemset(c->start[b].p, 0, sizeof(int) * c->start[b].cap));
     }
     const int ntile = (ncell + kScanTile - 1) / kScanTile;
-    const int ntile_sub = (int)((nsub + kScanTile - 1) / kScanTile);
-    CUDA_TRY(c, c->scan_state.reserve((size_t)ntile_sub));
+    CUDA_TRY(c, c->scan_state.reserve((size_t)ntile));
     CUDA_TRY(c, cudaMemset(c->count.p, 0, sizeof(int) * c->count.cap));
     CUDA_TRY(c, cudaMemset(c->scan_state.p, 0, sizeof(unsigned long long) * c->scan_state.cap));
     if (c->dist) {
@@ -1342,7 +1334,6 @@ void dpd_destroy(dpd_ctx *c)
         c->frc[b].release();
         c->start[b].release();
     }
-    c->sstart.release();
     c->rank_buf.release();
     c->count.release();
     c->scan_state.release();
@@ -1596,7 +1587,7 @@ int dpd_wall_carve(dpd_ctx *c, int32_t wall_species, int64_t *n_frozen, int64_t 
         if (renumber && hc[1] > 0) {
             const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
             TRY(launch(c, KID_GATHER, [&] {
-                k_scan<1><<<tiles, kScanThreads, 0, c->stream>>>(kbid.p, nid.p, n, tstate.p,
+                k_scan<<<tiles, kScanThreads, 0, c->stream>>>(kbid.p, nid.p, n, tstate.p,
                                                               reinterpret_cast<unsigned *>(epoch.p));
             }));
             TRY(launch(c, KID_GATHER, [&] {

@@ -87,9 +87,9 @@ __global__ void __launch_bounds__(256) k_bin_recv(Msgs rec, Geom g, int maxcap, 
         const float4 p = msg_data(rec, d)[2 * k];
         const float3 x = make_float3(p.x, p.y, p.z);
         if (!in_local_box(g, x)) raise_err(err, ERR_RANGE, __float_as_int(p.w));
-        else c = sub_index(g, p.x, p.y, p.z);
+        else c = cell_index(g, p.x, p.y, p.z);
     }
-    const int r = warp_rank_in_cell(count, c); // sub-bin counts, as k_bin
+    const int r = warp_rank_in_cell(count, c);
     if (k < cnt) rank_in[d * maxcap + k] = (c >= 0) ? r : -1;
 }
 
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) k_scatter_recv(Msgs rec, Geom g, int maxc
     const int r = rank_in[d * maxcap + k];
     if (r < 0) return;
     const float4 p = msg_data(rec, d)[2 * k], v = msg_data(rec, d)[2 * k + 1];
-    const int dst = start[sub_index(g, p.x, p.y, p.z)] + r; // start: the sub-bin starts
+    const int dst = start[cell_index(g, p.x, p.y, p.z)] + r;
     if (dst >= cap) { // more particles than the member's arrays hold: DPD_ERR_CAPACITY
         raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
         return;

@@ -59,7 +59,6 @@ constexpr int FT_NCUR = FT_NCUR_DEF;          // independent pair chains per lan
 #endif
 constexpr float FT_FAR = 1.0e18f;             // sentinel coordinate (its r^2 ~ 3e36 stays finite)
 constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32 owners + sentinel)
-constexpr int FT_SUBW = kSubX * FT_SX + 2;    // sub-bin table entries per staged row (+ end, even)
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
 struct FixP {
@@ -78,9 +77,6 @@ struct TileTab {
     int hoff[FT_NHROW + 1]; // home row -> first home index (prefix)
     int rend[FT_SY * FT_SZ]; // staged row -> end of its particles (the sentinel gap follows)
     int total;            // staged particles
-    // staged row -> smem start of each x sub-bin of its cells (kSubX per cell, row-major in x;
-    // entry kSubX * (cells of the row) is the row's end): the sweep's row windows
-    unsigned short ssub[FT_SY * FT_SZ][FT_SUBW];
 };
 
 struct ForceTileSmem {
@@ -486,8 +482,7 @@ struct TileGeo {
 // role 1 (another warp): one home row per lane (two loads: the home cells of a row are
 // contiguous in the extended grid) and their scan.
 __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const Geom &g,
-                                           const int *__restrict__ start, const int *__restrict__ sstart, int role,
-                                           int lane)
+                                           const int *__restrict__ start, int role, int lane)
 {
     const int x0 = G.x0, y0 = G.y0, z0 = G.z0, bx = G.bx, by = G.by, bz = G.bz;
     const int sxa = bx + 2, sya = by + 2, sza = bz + 1;
@@ -496,7 +491,7 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
     static_assert(FT_SY * FT_SZ <= 32 && FT_NHROW <= 32, "one lane per row");
     if (role == 0) {
         const int nrows = sya * sza;
-        int cnt[FT_SX], gst[FT_SX], sub[FT_SX][kSubX - 1], rsum = 0;
+        int cnt[FT_SX], gst[FT_SX], rsum = 0;
         if (lane < nrows) {
             const int lz = lane >= 2 * sya ? 2 : (lane >= sya ? 1 : 0); // sza <= 3
             const int ly = lane - lz * sya;
@@ -513,8 +508,6 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
                     gst[x] = start[gc];
                     cnt[x] = start[gc + 1] - gst[x];
                     rsum += cnt[x];
-#pragma unroll
-                    for (int k = 1; k < kSubX; ++k) sub[x][k - 1] = sstart[kSubX * gc + k];
                 }
             }
         }
@@ -527,15 +520,10 @@ __device__ __forceinline__ void tile_table(TileTab &T, const TileGeo &G, const G
                 if (x < sxa) {
                     T.soff[c0 + x] = run;
                     T.cgs[c0 + x] = gst[x];
-                    T.ssub[lane][kSubX * x] = (unsigned short)run;
-#pragma unroll
-                    for (int k = 1; k < kSubX; ++k)
-                        T.ssub[lane][kSubX * x + k] = (unsigned short)(run + sub[x][k - 1] - gst[x]);
                     run += cnt[x];
                 }
             }
             T.rend[lane] = run;
-            T.ssub[lane][kSubX * sxa] = (unsigned short)run;
             if (FT_ROWPAD) T.soff[c0 + sxa] = run; // segment ends never include the sentinel gap
         }
         const int tot = __shfl_sync(0xffffffffu, incl, 31) + FT_GAP * nrows;
@@ -624,6 +612,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
     //           sweep the lane's 5 segments into its list, then evaluate the warp's pairs
     //           with a warp-balanced split -- no CTA barrier between sweep and pairs
     const int rs = sxa + FT_ROWPAD; // table row stride
+    const int rowz = rs * sya;
     const float hx = g.L[0] / (float)g.n[0], hy = g.L[1] / (float)g.n[1], hz = g.L[2] / (float)g.n[2];
     const int wb = warp * FT_WSTRIDE;
     const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[tid * FT_LSTRIDE]);
@@ -642,10 +631,14 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             s_i = T.soff[crow + 1] + (h - T.hoff[r]);
             int lx = 1;
             while (lx < bx && T.soff[crow + lx + 1] <= s_i) ++lx;
+            const int c = crow + lx;
+            const int c1 = c - 1 + rs; // (lx - 1, ly + 1, lz): the y+1 row
             const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
-            // lower bounds (minus a rounding slack) on the distance from i to its cell's y / z
-            // faces: a row farther than r_c holds no partner, a nearer one a narrower window
-            const float oy = py - (float)(y0 + ly - 1) * hy, oz = pz - (float)(z0 + lz) * hz;
+            // row-end pruning: lower bounds (minus a rounding slack) on the distance from i
+            // to its cell's faces; a row / end cell farther than r_c holds no partner
+            const float ox = px - (float)(x0 + lx - 1) * hx, oy = py - (float)(y0 + ly - 1) * hy,
+                        oz = pz - (float)(z0 + lz) * hz;
+            const float dxl = fmaxf(ox - fx.slack, 0.0f), dxr = fmaxf(hx - ox - fx.slack, 0.0f);
             const float dyl = fmaxf(oy - fx.slack, 0.0f), dyr = fmaxf(hy - oy - fx.slack, 0.0f);
             const float dzr = fmaxf(hz - oz - fx.slack, 0.0f);
             unsigned lptr = lbase;
@@ -653,28 +646,14 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 #ifndef PROBE_NOSWEEP // timing probes: compile the sweep / pair walk out; wrong forces
 #define PROBE_NOSWEEP 0
 #endif
-            // Fused sweep.  The first aligned block of segment 0 (own cell after i, then the
-            // own row's window up to px + r_c) is the only masked one (j > i) and is peeled:
-            // every lane runs exactly one.  All later blocks are unmasked: a block running
-            // past a window end meets sub-bins beyond the window (farther than rc' in x, so
-            // beyond r_c) or the row's sentinels, and a block starting before a window start
-            // (aligned down) meets sub-bins before it or the previous row's sentinels; all of
-            // them fail the cutoff test.  The lane's remaining segments (rest of 0, then the
-            // four row windows) are one queue, walked by one loop, so a lane's trip count is
-            // its total block count.
+            // Fused sweep.  The first aligned block of segment 0 (own cell after i, next cell)
+            // is the only masked one (j > i) and is peeled: every lane runs exactly one.  All
+            // later blocks are unmasked: a block running past a segment end meets a cell two
+            // away (distance > h >= r_c) or the row's sentinels, which fail the cutoff test.
+            // The lane's remaining segments (rest of 0, then the pruned rows) are one queue,
+            // walked by one loop, so a lane's trip count is its total block count.
             const unsigned long long PX = f2dup(px), PY = f2dup(py), PZ = f2dup(pz);
-            // x windows (cells sorted by x sub-bin, kSubX per cell): in a row whose y / z
-            // faces are qy, qz away, a partner lies within rc' = sqrt(rc^2 - qy^2 - qz^2) of
-            // px in x; the window is the run of sub-bins overlapping [px - rc', px + rc']
-            // (widened by the slack that covers the binning's fp32 rounding), clamped to the
-            // row's three cells lx - 1 .. lx + 1.  Sub-bin u of the row covers tile-frame x in
-            // [(x0 - 1) hx + u hx / kSubX, ...).
-            const float inv_hs = (float)kSubX / hx, ub = (float)(kSubX * (x0 - 1));
-            const int umin = kSubX * (lx - 1), umax = kSubX * (lx + 2) - 1;
-            const int row_own = ly + sya * lz;
-            const float rcs = sqrt_approx(pp.rc2) + fx.slack;
-            const int u_own = min(max(__float2int_rd(__fmaf_rn(px + rcs, inv_hs, -ub)), umin), umax);
-            const int a0s = s_i + 1, b0s = T.ssub[row_own][u_own + 1];
+            const int a0s = s_i + 1, b0s = T.soff[c + 2];
             const int j0 = a0s & ~3;
             if (!PROBE_NOSWEEP && j0 < b0s) {
                 float ra, rb, rc, rd;
@@ -691,8 +670,9 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 #endif
 #pragma unroll
             for (int kk = 0; kk < 5; ++kk) {
-                // push-front order: FT_LOCKSTEP walks the four row windows first and the own
-                // row's rest last; else the own row first
+                // push-front order: FT_LOCKSTEP walks the four rows first, unpruned, so lanes
+                // of one cell read the same candidate quads together (shared-memory broadcast),
+                // and their own-cell rest last; else own-cell rest first, rows pruned
                 const int k = FT_LOCKSTEP ? (kk == 0 ? 0 : 5 - kk) : 4 - kk;
                 int a, b;
                 bool ne;
@@ -701,17 +681,13 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                     b = b0s;
                     ne = a < b;
                 } else {
-                    // k = 1: the y+1 row; 2..4: the z+1 rows at y - 1, y, y + 1
-                    const int row = (k == 1) ? row_own + 1 : row_own + sya + (k - 3);
-                    const float qy = (k == 2) ? dyl : ((k == 3) ? 0.0f : dyr);
+                    const int cs = (k == 1) ? c1 : c1 - 2 * rs + rowz + (k - 2) * rs;
+                    const float qy = (k == 2) ? dyl : (k == 3 ? 0.0f : dyr);
                     const float qz = (k == 1) ? 0.0f : dzr;
-                    const float r2w = pp.rc2 - __fmaf_rn(qy, qy, qz * qz);
-                    const float rw = sqrt_approx(fmaxf(r2w, 0.0f)) + fx.slack;
-                    const int ulo = max(__float2int_rd(__fmaf_rn(px - rw, inv_hs, -ub)), umin);
-                    const int uhi = min(__float2int_rd(__fmaf_rn(px + rw, inv_hs, -ub)), umax);
-                    a = T.ssub[row][ulo];
-                    b = T.ssub[row][uhi + 1];
-                    ne = r2w > 0.0f && a < b;
+                    const float q = qy * qy + qz * qz;
+                    a = (FT_LOCKSTEP || dxl * dxl + q < pp.rc2) ? T.soff[cs] : T.soff[cs + 1];
+                    b = (FT_LOCKSTEP || dxr * dxr + q < pp.rc2) ? T.soff[cs + 3] : T.soff[cs + 2];
+                    ne = (FT_LOCKSTEP || q < pp.rc2) && a < b;
                 }
                 if (PROBE_NOSWEEP) ne = false;
                 if (ne) {
@@ -871,7 +847,7 @@ __device__ __forceinline__ bool tile_overflows(const TileTab &T, const TileGeo &
 template <bool RECORD, int KMODE>
 __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     k_force_tile(const float4 *__restrict__ pos, const float4 *__restrict__ vel, float4 *__restrict__ frc,
-                 const int *__restrict__ start, const int *__restrict__ sstart, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
+                 const int *__restrict__ start, Geom g, PairP pp, FixP fx, const __grid_constant__ RoundKeys rk,
                  PairRec rec, int *err, float4 *__restrict__ fzero, int nzero)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -900,7 +876,7 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     G.by = min(FT_BY, g.n[1] - G.y0);
     G.bz = min(FT_BZ, g.n[2] - G.z0);
     TileTab &T = S.tab[0];
-    if (warp < 2) tile_table(T, G, g, start, sstart, warp, lane);
+    if (warp < 2) tile_table(T, G, g, start, warp, lane);
     __syncthreads();
     if (tile_overflows(T, G)) {
         if (tid == 0) atomicAdd(&err[T.total > FT_SCAP ? 4 : 5], 1); // fallback statistics

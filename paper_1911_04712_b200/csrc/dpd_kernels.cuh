@@ -44,21 +44,6 @@ __device__ __forceinline__ int cell_index(const Geom &g, float x, float y, float
     return ix + g.ext[0] * (iy + g.ext[1] * iz);
 }
 
-// Sort key of the cell list: the cell of (x, y, z) refined into kSubX bins along x (the bin
-// of x inside its cell, from the same fp32 product x * inv_h as cell_coord, clamped into the
-// cell).  Sorting by it keeps every cell contiguous (start[c] = sstart[kSubX c]) and orders
-// each row of cells by x to 1/kSubX of a cell, so the force sweep can window a neighbour
-// row to the x-range a particle can reach (dpd_force_tile.cuh).
-constexpr int kSubX = 4;
-
-__device__ __forceinline__ int sub_index(const Geom &g, float x, float y, float z)
-{
-    const float fx = __fmul_rn(x, g.inv_h[0]);
-    const int cx = min(max(__float2int_rz(fx), 0), g.n[0] - 1);
-    const int xs = min(max(__float2int_rz(__fmul_rn(fx - (float)cx, (float)kSubX)), 0), kSubX - 1);
-    return cell_index(g, x, y, z) * kSubX + xs;
-}
-
 // Body force along z: periodic Poiseuille, or uniform (wall-bounded flows).
 __device__ __forceinline__ float body_fz(const IntegP &ip, float x_local)
 {
@@ -329,10 +314,10 @@ __global__ void __launch_bounds__(256, 8) k_bin(const float4 *__restrict__ pos, 
                 raise_err(err, finite3(un.x, un.y, un.z) ? ERR_RANGE : ERR_NONFINITE, __float_as_int(p.w));
                 xn = make_float3(0.0f, 0.0f, 0.0f);
             }
-            c = sub_index(g, xn.x, xn.y, xn.z);
+            c = cell_index(g, xn.x, xn.y, xn.z);
         }
     }
-    const int r = warp_rank_in_cell(count, c); // rank within the x sub-bin of the cell
+    const int r = warp_rank_in_cell(count, c);
     if (i < n) rank[i] = (c >= 0) ? r : -1;
 }
 
@@ -353,14 +338,10 @@ __device__ __forceinline__ unsigned long long scan_pack(unsigned epoch, int flag
     return ((unsigned long long)((epoch << 2) | (unsigned)flag) << 32) | (unsigned)value;
 }
 
-// SUB > 1: count holds ncell = SUB x cells sub-bin counts; start receives the sub-bin starts
-// and cstart the cell starts (cstart[c] = start[SUB c], cstart[ncell / SUB] = total).
-template <int SUB = 1>
 __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, int *__restrict__ start,
                                                        int ncell, unsigned long long *tstate,
-                                                       unsigned *epoch_ptr, int *__restrict__ cstart = nullptr)
+                                                       unsigned *epoch_ptr)
 {
-    static_assert(SUB == 1 || (SUB == 4 && kScanItems == 16), "one int4 of cell starts per 16 sub-bin items");
     __shared__ int warp_sums[kScanThreads / 32];
     __shared__ int tile_prefix;
     __shared__ unsigned s_epoch;
@@ -446,7 +427,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, 
     if (base + kScanItems <= ncell) {
         int4 *dst = reinterpret_cast<int4 *>(start + base);
         int4 *cz = reinterpret_cast<int4 *>(count + base);
-        int cs[kScanItems / 4];
 #pragma unroll
         for (int q = 0; q < kScanItems / 4; ++q) {
             int4 o;
@@ -456,10 +436,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, 
             o.w = excl; excl += v[4 * q + 3];
             dst[q] = o;
             cz[q] = make_int4(0, 0, 0, 0);
-            cs[q] = o.x;
-        }
-        if constexpr (SUB == 4) { // items base .. base + 15 are cells base / 4 .. base / 4 + 3
-            reinterpret_cast<int4 *>(cstart + base / 4)[0] = make_int4(cs[0], cs[1], cs[2], cs[3]);
         }
     } else {
 #pragma unroll
@@ -467,16 +443,12 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(int *__restrict__ count, 
             if (base + k < ncell) {
                 start[base + k] = excl;
                 count[base + k] = 0;
-                if (SUB > 1 && (base + k) % SUB == 0) cstart[(base + k) / SUB] = excl;
             }
             excl += v[k];
         }
     }
     if (tile == gridDim.x - 1) {
-        if (t == kScanThreads - 1) {
-            start[ncell] = tile_prefix + total;
-            if (SUB > 1) cstart[ncell / SUB] = tile_prefix + total;
-        }
+        if (t == kScanThreads - 1) start[ncell] = tile_prefix + total;
         if (t == 0) *((volatile unsigned *)epoch_ptr) = epoch; // every tile has read it by now
     }
 }
@@ -499,7 +471,8 @@ __global__ void __launch_bounds__(256) k_scatter(const float4 *__restrict__ pos,
     advance<LEAN>(g, ip, p, v, f, xn, un);
     if (!finite3(xn.x, xn.y, xn.z) || !finite3(un.x, un.y, un.z) || !in_local_box(g, xn))
         xn = make_float3(0.0f, 0.0f, 0.0f);
-    const int dst = start[sub_index(g, xn.x, xn.y, xn.z)] + rank[i]; // start: the sub-bin starts
+    const int c = cell_index(g, xn.x, xn.y, xn.z);
+    const int dst = start[c] + rank[i];
     if (dst >= cap) { // a decomposed member gained more particles than its arrays hold
         raise_err(err, ERR_CAPACITY, __float_as_int(p.w));
         return;
