@@ -37,6 +37,9 @@ UNIT = "particle-steps/s"
 BYTES_PER_PARTICLE_STEP = 192.0  # bin 56 + scan ~1 + scatter 88 + force 48 (rounded model)
 
 
+_RESULT_OUT = sys.stdout  # main() re-points it at a duplicate of the original fd 1
+
+
 def rank_grid(n):
     return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(n) or _factor3(n)
 
@@ -264,7 +267,7 @@ def run_reference(args, cfg):
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out), file=_RESULT_OUT, flush=True)
     return 0
 
 
@@ -292,11 +295,18 @@ def rank_particles(cfg, world, rank, scaling="weak"):
     return pos, vel, ids, coord, sub
 
 
-def weak_point(capi, stream, torch, steps, warmup):
+def weak_point(capi, stream, torch, steps, warmup, loopback=False):
     """BASELINE config 4 (128^3, rho = 8) on this one GPU: particle-steps/s over `steps`
-    device-timed steps after `warmup`, inputs resident."""
+    device-timed steps after `warmup`, inputs resident.  loopback: the same box as ONE
+    subdomain of a 3D decomposition whose six faces are exchanged through NCCL with the rank
+    itself (dpd_create_loopback: ghost pack, NCCL send/recv, ghost sort and halo forces,
+    migration) -- the per-GPU step of the 8-GPU weak series, on one GPU."""
     cfg = workloads.CONFIGS["weak128"]
-    ctx = capi.dpd_create(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
+    if loopback:
+        ctx = capi.dpd_create_loopback(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed,
+                                       (1, 1, 1))
+    else:
+        ctx = capi.dpd_create(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed)
     try:
         capi.dpd_set_stream(ctx, stream.cuda_stream)
         pos, vel = workloads.make_config(cfg)
@@ -309,6 +319,11 @@ def weak_point(capi, stream, torch, steps, warmup):
         e1.record(stream)
         capi.dpd_sync(ctx)
         ms = e0.elapsed_time(e1)
+        if loopback:
+            return {"value": cfg.n * steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+                    "workload": "weak128 as one subdomain of a 3D decomposition (split x, y, z), all six faces "
+                                "exchanged through NCCL send/recv with the rank itself (dpd_create_loopback): "
+                                "the per-GPU step of the N = 8 weak-scaling line without the NVLink transfer time"}
         return {"value": cfg.n * steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
                 "workload": "weak128: 128^3 rho=8 (16,777,216 particles), BASELINE config 4 on one GPU -- the "
                             "per-GPU workload of the N > 1 weak-scaling lines"}
@@ -350,6 +365,13 @@ def main():
     if args.oracle_probe:
         oracle_probe(args.oracle_probe)
         return 0
+    # stdout carries exactly one JSON line: native code writes to fd 1 on its own (NCCL's
+    # version banner at communicator init), so fd 1 points at stderr for the run and the
+    # result line goes through a private duplicate of the original stdout
+    global _RESULT_OUT
+    sys.stdout.flush()
+    _RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args.warmup = max(args.warmup, 3)
     if args.config is None:
         args.config = "eq64" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "weak128"
@@ -525,6 +547,11 @@ def main():
     # config-4 workload on this one GPU, same timing rules, is recorded beside it
     if world == 1 and args.config == "eq64" and not args.no_weak_point:
         out["weak128_n1"] = weak_point(capi, stream, torch, max(5, min(args.steps, 20)), args.warmup)
+        try:
+            out["weak128_loopback_n1"] = weak_point(capi, stream, torch, max(5, min(args.steps, 20)), args.warmup,
+                                                    loopback=True)
+        except Exception as exc:  # noqa: BLE001  (a library built without NCCL)
+            out["weak128_loopback_n1"] = {"error": repr(exc)}
 
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -532,7 +559,7 @@ def main():
         except Exception as exc:  # noqa: BLE001
             out["cpu_baseline"] = {"error": repr(exc)}
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=_RESULT_OUT, flush=True)
     capi.dpd_destroy(ctx)
     if world > 1:
         dist.destroy_process_group()
