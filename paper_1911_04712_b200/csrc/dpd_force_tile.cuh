@@ -618,8 +618,18 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
     const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[tid * FT_LSTRIDE]);
     // warp w owns home particles [w nhome / NWARP, (w + 1) nhome / NWARP): equal counts, so
     // no warp idles at the flush barrier for want of particles
+#ifndef FT_CHUNK32
+#define FT_CHUNK32 0
+#endif
+#if FT_CHUNK32
+    // warp w owns the full 32-particle chunks w, w + NWARP, ...: every sweep lane busy but in
+    // the last chunk (an idle warp costs no issue slots, an idle lane does)
+    const int hend = nhome;
+    for (int hb = warp * 32; hb < hend; hb += 32 * FT_NWARP) {
+#else
     const int hend = ((warp + 1) * nhome) / FT_NWARP;
     for (int hb = (warp * nhome) / FT_NWARP; hb < hend; hb += 32) {
+#endif
         const int h = hb + lane;
         int cnt = 0, s_i = 0;
         if (h < hend) {

@@ -40,3 +40,22 @@ def test_upper_face_rounding_is_kept_local():
     cfg = workloads.CONFIGS["weak128"]
     pos = bench.rank_particles(cfg, 8, 7, "weak")[0]
     assert np.all(pos < np.float32(256.0)) and np.all(pos >= np.float32(128.0))
+
+
+def test_reference_arm_prints_exactly_one_json_line():
+    """The driver parses bench.py's stdout as ONE JSON line: everything else (native
+    libraries writing to fd 1, progress) must go to stderr.  The reference arm (the CPU
+    oracle) runs here without a GPU."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, res.stdout[:2000]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["steps"] == 1 and d["warmup"] == 3 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"

@@ -1,7 +1,8 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
 config-1 box on one domain (the tiled and the reference force kernel), the species matrix,
 asynchronous dumps (snapshot kernel + copy stream + writer thread) and a 2x2x2 in-process
-group, serialised and as the production task graph (comm streams, CUDA events)."""
+group, serialised and as the production task graph (comm streams, CUDA events); with
+SANITIZE_LOOPBACK=1 also the one-rank NCCL loopback context (split x, y, z)."""
 import tempfile
 import os
 import sys
@@ -50,4 +51,10 @@ for graph in (0, 1):
     capi.dpd_group_step(ctxs, 3)
     for c in ctxs:
         capi.dpd_destroy(c)
+if os.environ.get("SANITIZE_LOOPBACK") == "1":
+    c = capi.dpd_create_loopback(big.box, big.rc, big.a, big.gamma, big.kT, big.power, big.dt, big.seed, (1, 1, 1))
+    capi.dpd_set_particles_ex(c, p2, v2, np.arange(p2.shape[0], dtype=np.int32), 0)
+    capi.dpd_step(c, 3)
+    capi.dpd_get_state(c)
+    capi.dpd_destroy(c)
 print("sanitize run ok")
