@@ -616,14 +616,14 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
     const float hx = g.L[0] / (float)g.n[0], hy = g.L[1] / (float)g.n[1], hz = g.L[2] / (float)g.n[2];
     const int wb = warp * FT_WSTRIDE;
     const unsigned lbase = (unsigned)__cvta_generic_to_shared(&S.lst[tid * FT_LSTRIDE]);
-    // warp w owns home particles [w nhome / NWARP, (w + 1) nhome / NWARP): equal counts, so
-    // no warp idles at the flush barrier for want of particles
 #ifndef FT_CHUNK32
-#define FT_CHUNK32 0
+#define FT_CHUNK32 1
 #endif
 #if FT_CHUNK32
     // warp w owns the full 32-particle chunks w, w + NWARP, ...: every sweep lane busy but in
-    // the last chunk (an idle warp costs no issue slots, an idle lane does)
+    // the last chunk -- an idle warp costs no issue slots, an idle lane does (round 2: 396.5 ->
+    // 390.6 us against equal counts per warp, [w nhome / NWARP, (w + 1) nhome / NWARP), which
+    // left ~11 % of the sweep's lanes idle; profiles/r02d_ab_chunk32.jsonl)
     const int hend = nhome;
     for (int hb = warp * 32; hb < hend; hb += 32 * FT_NWARP) {
 #else
