@@ -17,9 +17,11 @@
 //                unmasked 4-aligned blocks: a block running past a segment meets cells two
 //                away or sentinels, both beyond r_c.  One LDS.128 per coordinate, packed
 //                fp32x2 distance math (FADD2/FFMA2), one predicated 16-bit store + add per hit;
-//   4. pairs   : the warp's lists are concatenated and cut into 32 contiguous lane chunks,
-//                each walked by two cursors (two Philox/Box-Muller chains in flight); the
-//                i-side sum stays in registers until the owner changes;
+//   4. pairs   : phase A -- every lane walks the first FT_PHASEA entries of its own list
+//                (owner = its home particle, no owner switches); phase B -- the leftovers of
+//                the warp's lists are concatenated and cut into 32 contiguous lane chunks,
+//                each walked by one cursor; the i-side sum stays in registers until the
+//                owner changes;
 //   5. accumulate: a, gamma, sigma are pre-scaled by the power-of-two fixed-point scale, so
 //                one FFMA quantises each force component; native shared-memory integer
 //                atomics (+q on i, -q on j): exact Newton-3, order-independent sums;
@@ -653,6 +655,10 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             const float dzr = fmaxf(hz - oz - fx.slack, 0.0f);
             unsigned lptr = lbase;
             bool full = false;
+#ifndef PROBE_NOPAIR
+#define PROBE_NOPAIR 0
+#endif
+#define PROBE_NOPAIR_A PROBE_NOPAIR
 #ifndef PROBE_NOSWEEP // timing probes: compile the sweep / pair walk out; wrong forces
 #define PROBE_NOSWEEP 0
 #endif
@@ -763,23 +769,62 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             cnt = (int)(lptr - lbase) >> 1;
         }
 
-        // ---- 3. the warp's compacted owner table: one packed scan (owners | entries << 8)
-        const int v = (cnt > 0 ? 1 : 0) | (cnt << 8);
+#ifndef FT_PHASEA
+#define FT_PHASEA 10
+#endif
+        // ---- 3a. phase A: every lane walks the first FT_PHASEA entries of its OWN list (the
+        //          owner is the lane's home particle: no owner switches, i-side sums in
+        //          registers); the ~ (cnt - FT_PHASEA)+ leftovers are balanced in phase B.
+        //          Round 2 (profiles/r02e_ab_phasea.jsonl): 390.6 us without phase A, 388.2 /
+        //          387.5 / 386.9 / 387.5 / 389.6 us with 6 / 8 / 10 / 12 / 14, 389.8 with the
+        //          warp's shortest list -- the owner-switch blocks of the balanced walk ran at
+        //          ~2 lanes in 78 % of its iterations
+        // FT_PHASEA < 0: phase A takes the warp's shortest list length (every lane busy)
+        const int pa = FT_PHASEA >= 0 ? FT_PHASEA : (int)__reduce_min_sync(0xffffffffu, (unsigned)(h < hend ? cnt : 1 << 20));
+        if (FT_PHASEA != 0 && !PROBE_NOPAIR_A) {
+            const int na = min(cnt, pa);
+            const int namax = __reduce_max_sync(0xffffffffu, na);
+            if (namax > 0) {
+                const int lrow = tid * FT_LSTRIDE;
+                const float px = S.sx[s_i], py = S.sy[s_i], pz = S.sz[s_i];
+                const float4 vi = S.sv[s_i];
+                AccT ax = 0, ay = 0, az = 0;
+                float amax = 0.0f;
+                for (int t = 0; t < namax; ++t) {
+                    if (t < na) {
+                        const int j = S.lst[lrow + t];
+                        const float4 vj = S.sv[j];
+                        float dx, dy, dz;
+                        const float sv = pair_core<KMODE>(pp, px, py, pz, vi, S.sx[j], S.sy[j], S.sz[j], vj, ks, dx, dy,
+                                                          dz, amax);
+                        if constexpr (RECORD) pair_record<KMODE>(vi, vj, dx, dy, dz, ks, rec);
+                        const AccT qx = acc_q(dx, sv), qy = acc_q(dy, sv), qz = acc_q(dz, sv);
+                        ax += qx;
+                        ay += qy;
+                        az += qz;
+                        acc_add(S, frc, j, -qx, -qy, -qz);
+                    }
+                }
+                if (na > 0 && (ax != 0 || ay != 0 || az != 0)) acc_add(S, frc, s_i, ax, ay, az);
+                if (amax > fx.mag_lim * fx.scale) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(vi.w));
+            }
+        }
+        const int cnt_b = max(cnt - pa, 0);
+        // ---- 3. the warp's compacted owner table of the phase-B leftovers: one packed scan
+        //         (owners | entries << 8)
+        const int v = (cnt_b > 0 ? 1 : 0) | (cnt_b << 8);
         const int incl = warp_incl_scan(v, lane);
         const int tp = __shfl_sync(0xffffffffu, incl, 31);
         const int nown = tp & 0xFF, tot = tp >> 8;
-        if (cnt > 0) {
+        if (cnt_b > 0) {
             const int o = (incl - v) & 0xFF, e = (incl - v) >> 8;
-            S.wrec[wb + o] = make_int4(e, e + cnt, tid * FT_LSTRIDE - e, s_i);
+            S.wrec[wb + o] = make_int4(e, e + cnt_b, tid * FT_LSTRIDE + pa - e, s_i);
         }
         __syncwarp();
 
         // ---- 4. pair evaluation: contiguous chunk of the warp's lists per lane, walked by two
         //         independent cursors (halves of the chunk) so two Philox/Box-Muller chains
         //         are in flight per thread (instruction-level parallelism)
-#ifndef PROBE_NOPAIR
-#define PROBE_NOPAIR 0
-#endif
         if (tot > 0 && !PROBE_NOPAIR) {
             const int C = (tot + 31) >> 5;
             const int t0 = min(lane * C, tot);
