@@ -587,8 +587,9 @@ int phase_ghost_sort(dpd_ctx *c, cudaStream_t st)
 }
 
 // a9 (second half): one-sided local-ghost forces (after the local forces, same stream).
-int phase_halo_force(dpd_ctx *c, int64_t step)
+int phase_halo_force(dpd_ctx *c, int64_t step, cudaStream_t st = nullptr)
 {
+    if (!st) st = c->stream;
     const Geom g = c->geom;
     const uint32_t s_lo = (uint32_t)(uint64_t)step, s_hi = (uint32_t)((uint64_t)step >> 32);
     const PairP pp = c->pp;
@@ -597,7 +598,7 @@ int phase_halo_force(dpd_ctx *c, int64_t step)
         // grid-stride over the boundary list (its length lives on the device)
         const unsigned nbh = (unsigned)c->nsm * 16; // grid-stride over the boundary cells (count on device)
 #define DPD_HALO(K)                                                                                                 \
-    k_force_halo_cells<K><<<nbh, 32 * kHcWarps, 0, c->stream>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, c->blist.p,  \
+    k_force_halo_cells<K><<<nbh, 32 * kHcWarps, 0, st>>>(c->pos[b].p, c->vel[b].p, c->frc[b].p, c->blist.p,  \
                                                                 c->start[c->scur].p, c->gpos.p, c->gvel.p,          \
                                                                 c->gstart.p, g, pp, c->fix.scale, c->fix.inv_scale, \
                                                                 c->fix.mag_lim, s_lo, s_hi, c->err.p)
@@ -608,7 +609,7 @@ int phase_halo_force(dpd_ctx *c, int64_t step)
         default: DPD_HALO(3); break;
         }
 #undef DPD_HALO
-    });
+    }, st);
 }
 
 // a9 on the context's stream (prime, in-process group).
@@ -884,8 +885,9 @@ int dump_copyout(dpd_ctx *c, cudaStream_t st)
 
 // ---- one step of one context as a task graph (NCCL or single) ----------------------------
 // Tasks (stream slot): kick_drift_bin (0) -> [migrate_exchange (0)] -> scan_scatter (0) ->
-// [ghost_pack -> ghost_exchange -> ghost_sort (all 1, comm stream)] ; force_local (0) ->
-// [halo_force (0), after ghost_sort] -> [snapshot (0) -> snapshot_d2h (2, copy stream)].  Kahn's order
+// [ghost_pack -> ghost_exchange -> ghost_sort -> halo_force (all 1, comm stream)] ; force_local
+// (0) -> [join (0), after force_local and halo_force] -> [snapshot (0) -> snapshot_d2h (2, copy
+// stream)].  Kahn's order
 // issues ghost_exchange before force_local, so the exchange overlaps the interior forces
 // (P:244-247); cross-stream edges become CUDA events.
 dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
@@ -924,10 +926,15 @@ dpd::TaskGraph *build_step_graph(dpd_ctx *c, bool with_dump)
     g->edge(t_sort, t_force);
     last = t_force;
     if (c->dist) {
-        const int t_h = g->add("halo_force", 0, [c](cudaStream_t) { return phase_halo_force(c, c->step); });
-        g->edge(t_force, t_h);
+        // the halo forces run on the communication stream right after the ghost sort,
+        // concurrent with the interior force pass: both add into the step's force array with
+        // vector reductions; the step ends when both are done (join on the compute stream)
+        const int t_h = g->add("halo_force", 1, [c](cudaStream_t s) { return phase_halo_force(c, c->step, s); });
         g->edge(t_gx, t_h);
-        last = t_h;
+        const int t_j = g->add("join", 0, nullptr);
+        g->edge(t_force, t_j);
+        g->edge(t_h, t_j);
+        last = t_j;
     }
     if (with_dump) {
         const int t_s = g->add("snapshot", 0, [c](cudaStream_t s) { return dump_snapshot(c, s); });

@@ -422,12 +422,11 @@ __global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps pe
                 if (qn > 0) evaluate(qn);
             }
             __syncwarp();
-            if (lane < ni) {
-                float4 f = frc[s0 + ib + lane];
-                f.x += (float)acc[warp][0][lane] * inv_scale;
-                f.y += (float)acc[warp][1][lane] * inv_scale;
-                f.z += (float)acc[warp][2][lane] * inv_scale;
-                frc[s0 + ib + lane] = f;
+            if (lane < ni) { // a vector reduction: the interior force kernel may still be adding
+                const int ax = acc[warp][0][lane], ay = acc[warp][1][lane], az = acc[warp][2][lane];
+                if (ax | ay | az)
+                    atomicAdd(&frc[s0 + ib + lane],
+                              make_float4((float)ax * inv_scale, (float)ay * inv_scale, (float)az * inv_scale, 0.0f));
             }
             __syncwarp();
         }

@@ -118,8 +118,9 @@ def test_dumps_overlap_compute_on_a_slow_disk(tmp_path):
 def test_step_schedule_decomposed():
     """The step graph of a decomposed context (what the NCCL path runs; printed from a member
     of an in-process group, whose contexts are split the same way): the ghost exchange and the
-    ghost pack, exchange and binning are issued on the communication stream before the local
-    forces, so they overlap them, and the halo forces wait for both."""
+    ghost pack, exchange, binning and the halo forces are issued on the communication stream
+    before / beside the local forces, so they overlap them; the step ends
+    with a join of both streams."""
     from paper_1911_04712_b200 import capi
     cfg = workloads.with_box(workloads.CONFIGS["parity"], (12.0, 12.0, 12.0))
     ctxs = capi.dpd_create_group(cfg.box, cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed, (2, 1, 1))
@@ -127,15 +128,16 @@ def test_step_schedule_decomposed():
         sched = capi.dpd_step_schedule(ctxs[0])
         names = [t[1] for t in sched]
         assert names == ["kick_drift_bin", "migrate_exchange", "scan_scatter", "ghost_pack", "ghost_exchange",
-                         "ghost_sort", "force_local", "halo_force"]
+                         "ghost_sort", "force_local", "halo_force", "join"]
         slot = {t[1]: t[0] for t in sched}
         preds = {t[1]: set(t[2]) for t in sched}
-        comm = ("ghost_pack", "ghost_exchange", "ghost_sort")
+        comm = ("ghost_pack", "ghost_exchange", "ghost_sort", "halo_force")
         assert all(slot[k] == 1 for k in comm)
         assert all(slot[k] == 0 for k in names if k not in comm)
         assert preds["ghost_sort"] == {"ghost_exchange"} and preds["ghost_exchange"] == {"ghost_pack"}
         assert preds["ghost_pack"] == {"scan_scatter"}
-        assert preds["halo_force"] == {"force_local", "ghost_sort"}
+        assert preds["halo_force"] == {"ghost_sort"}
+        assert preds["join"] == {"force_local", "halo_force"}
         assert preds["force_local"] == {"scan_scatter"}
     finally:
         for c in ctxs:

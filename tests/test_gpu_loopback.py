@@ -58,6 +58,7 @@ def test_loopback_prime_and_per_step_parity(split):
         check_forces(f_id, F_ref, allow)
         sched = {name: slot for slot, name, _ in capi.dpd_step_schedule(c)}
         assert sched["migrate_exchange"] == 0 and sched["ghost_exchange"] == 1 and sched["force_local"] == 0
+        assert sched["halo_force"] == 1 and sched["join"] == 0  # halo forces beside the interior ones
         for s in range(1, 31):
             capi.dpd_step(c, 1)
             pos, u, f, ids = capi.dpd_get_state(c)
