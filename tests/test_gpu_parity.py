@@ -567,6 +567,48 @@ def test_tiled_pair_set_equals_reference_kernel(box, rc, rho):
     assert capi.dpd_get_stat(d.ctx, "fallback_tiles") == 0
 
 
+def test_crowded_tiles_second_round_pair_set():
+    """rho = 9.2: a 4 x 4 x 2 tile holds ~294 home particles (sd 17), so most tiles have more
+    than the 9 x 32 = 288 that one round of warp chunks covers and warp 0 sweeps and walks a
+    second chunk; ~10 % of the tiles exceed the staging capacity and take the global-memory
+    fallback instead.  The pair set must still equal the reference kernel's (no duplicate,
+    none missing) and the forces the oracle's, over 20 steps."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.Config("crowded", (8.0, 8.0, 12.0), 9.2, 25.0, 4.5, 1.0, 0.5, 0.005)
+    p = _params(cfg)
+    pos0, vel0 = workloads.make_config(cfg)
+    d = _ctx(cfg, kernel=0)
+    d.set_particles(pos0, vel0)
+    L = np.array(cfg.box)
+    for s in range(21):
+        if s % 10 == 0:
+            sets = []
+            for kern in (0, 1):
+                d.set_option("force_kernel", kern)
+                q = d.debug_pairs()
+                key = q[:, 0].astype(np.int64) * (1 << 32) + q[:, 1].astype(np.int64)
+                assert len(np.unique(key)) == len(key), f"kernel {kern}: duplicate pair at step {s}"
+                sets.append(key)
+            d.set_option("force_kernel", 0)
+            diff = np.setxor1d(sets[0], sets[1])
+            if diff.size:
+                pos, _, _, ids = d.get_state()
+                x = np.empty_like(pos, dtype=np.float64)
+                x[ids] = pos
+                dr = x[diff >> 32] - x[diff & 0xFFFFFFFF]
+                dr -= L * np.round(dr / L)
+                assert np.all(np.abs((dr * dr).sum(axis=1) - 1.0) < 1e-4)
+            x, u, f, ids = d.get_state()
+            x_id, u_id, f_id = by_id(ids, x, u, f)
+            F_ref, allow, _ = oracle.forces(p, x_id, u_id, s, **window_kw(cfg.box))
+            check_forces(f_id, F_ref, allow)
+        if s < 20:
+            d.step(1)
+    ntiles = 2 * 2 * 6
+    fb = capi.dpd_get_stat(d.ctx, "fallback_tiles")
+    assert fb < 21 * ntiles // 2, "the tiled path must carry most tiles"
+
+
 def test_kernel_switch_keeps_force_buffers_consistent():
     """The sort's target force buffer is zeroed a step ahead: by the tiled kernel's first wave,
     or by a memset when the reference kernel computes the step.  Alternating the two kernels
