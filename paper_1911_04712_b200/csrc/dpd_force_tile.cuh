@@ -61,6 +61,17 @@ constexpr int FT_NCUR = FT_NCUR_DEF;          // independent pair chains per lan
 #endif
 constexpr float FT_FAR = 1.0e18f;             // sentinel coordinate (its r^2 ~ 3e36 stays finite)
 constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32 owners + sentinel)
+#ifndef FT_PA_UNROLL
+#define FT_PA_UNROLL 1
+#endif
+#ifndef FT_SW_UNROLL
+#define FT_SW_UNROLL 1
+#endif
+#ifndef FT_PA2
+#define FT_PA2 1
+#endif
+constexpr int kFtPaUnroll = FT_PA_UNROLL;     // unroll of the phase-A pair loop (1: none)
+constexpr int kFtSwUnroll = FT_SW_UNROLL;     // unroll of the sweep loop (1: none)
 
 // Fixed-point force quantisation: q = rint(f * scale), |f * scale| < 2^21 enforced.
 struct FixP {
@@ -720,7 +731,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             q2 = q3;
             q3 = q4;
             q4 = 0;
-#pragma unroll 1
+#pragma unroll kFtSwUnroll
             while (j < hi) {
                 if ((int)(lptr - lbase) > 2 * (FT_LCAP - 4)) { // list full (~4 sigma): the rest in place
                     full = true;
@@ -790,6 +801,35 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 const float4 vi = S.sv[s_i];
                 AccT ax = 0, ay = 0, az = 0;
                 float amax = 0.0f;
+#if FT_PA2
+                // two entries per iteration, predicated (an inactive slot evaluates the self pair:
+                // r2 = 0 -> f = 0, and skips its j-side atomics): two independent Philox /
+                // Box-Muller chains in flight (v65: 386.9 -> 381.6 us, 56 -> 64 registers; a
+                // loop unrolled by the compiler gave 386.2, the sweep unrolled 387.3, two
+                // cursors in phase B again 389.8; profiles/r02f_ab_phasea2.jsonl)
+                for (int t = 0; t < namax; t += 2) {
+                    const bool a0 = t < na, a1 = t + 1 < na;
+                    const int j0 = a0 ? (int)S.lst[lrow + t] : s_i, j1 = a1 ? (int)S.lst[lrow + t + 1] : s_i;
+                    const float4 v0 = S.sv[j0], v1 = S.sv[j1];
+                    float dx0, dy0, dz0, dx1, dy1, dz1;
+                    const float s0 = pair_core<KMODE>(pp, px, py, pz, vi, S.sx[j0], S.sy[j0], S.sz[j0], v0, ks, dx0,
+                                                      dy0, dz0, amax);
+                    const float s1 = pair_core<KMODE>(pp, px, py, pz, vi, S.sx[j1], S.sy[j1], S.sz[j1], v1, ks, dx1,
+                                                      dy1, dz1, amax);
+                    if constexpr (RECORD) {
+                        if (a0) pair_record<KMODE>(vi, v0, dx0, dy0, dz0, ks, rec);
+                        if (a1) pair_record<KMODE>(vi, v1, dx1, dy1, dz1, ks, rec);
+                    }
+                    const AccT qx0 = acc_q(dx0, s0), qy0 = acc_q(dy0, s0), qz0 = acc_q(dz0, s0);
+                    const AccT qx1 = acc_q(dx1, s1), qy1 = acc_q(dy1, s1), qz1 = acc_q(dz1, s1);
+                    ax += qx0 + qx1;
+                    ay += qy0 + qy1;
+                    az += qz0 + qz1;
+                    if (a0) acc_add(S, frc, j0, -qx0, -qy0, -qz0);
+                    if (a1) acc_add(S, frc, j1, -qx1, -qy1, -qz1);
+                }
+#else
+#pragma unroll kFtPaUnroll
                 for (int t = 0; t < namax; ++t) {
                     if (t < na) {
                         const int j = S.lst[lrow + t];
@@ -805,6 +845,7 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                         acc_add(S, frc, j, -qx, -qy, -qz);
                     }
                 }
+#endif
                 if (na > 0 && (ax != 0 || ay != 0 || az != 0)) acc_add(S, frc, s_i, ax, ay, az);
                 if (amax > fx.mag_lim * fx.scale) raise_err(err, ERR_RANGE, (int)w_id<KMODE>(vi.w));
             }
