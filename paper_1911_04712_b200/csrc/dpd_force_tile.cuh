@@ -70,6 +70,9 @@ constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32
 #ifndef FT_PA2
 #define FT_PA2 1
 #endif
+#ifndef FT_PAW
+#define FT_PAW 2 // phase-A entries per iteration (FT_PA2)
+#endif
 constexpr int kFtPaUnroll = FT_PA_UNROLL;     // unroll of the phase-A pair loop (1: none)
 constexpr int kFtSwUnroll = FT_SW_UNROLL;     // unroll of the sweep loop (1: none)
 
@@ -806,27 +809,37 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 // r2 = 0 -> f = 0, and skips its j-side atomics): two independent Philox /
                 // Box-Muller chains in flight (v65: 386.9 -> 381.6 us, 56 -> 64 registers; a
                 // loop unrolled by the compiler gave 386.2, the sweep unrolled 387.3, two
-                // cursors in phase B again 389.8; profiles/r02f_ab_phasea2.jsonl)
-                for (int t = 0; t < namax; t += 2) {
-                    const bool a0 = t < na, a1 = t + 1 < na;
-                    const int j0 = a0 ? (int)S.lst[lrow + t] : s_i, j1 = a1 ? (int)S.lst[lrow + t + 1] : s_i;
-                    const float4 v0 = S.sv[j0], v1 = S.sv[j1];
-                    float dx0, dy0, dz0, dx1, dy1, dz1;
-                    const float s0 = pair_core<KMODE>(pp, px, py, pz, vi, S.sx[j0], S.sy[j0], S.sz[j0], v0, ks, dx0,
-                                                      dy0, dz0, amax);
-                    const float s1 = pair_core<KMODE>(pp, px, py, pz, vi, S.sx[j1], S.sy[j1], S.sz[j1], v1, ks, dx1,
-                                                      dy1, dz1, amax);
-                    if constexpr (RECORD) {
-                        if (a0) pair_record<KMODE>(vi, v0, dx0, dy0, dz0, ks, rec);
-                        if (a1) pair_record<KMODE>(vi, v1, dx1, dy1, dz1, ks, rec);
+                // cursors in phase B again 389.8; three / four entries per iteration 381.3 /
+                // 383.0 us at 68 / 69 registers; profiles/r02f_ab_phasea2.jsonl)
+                for (int t = 0; t < namax; t += FT_PAW) {
+                    bool a[FT_PAW];
+                    int jj[FT_PAW];
+                    float4 vv[FT_PAW];
+                    float sv[FT_PAW], dx[FT_PAW], dy[FT_PAW], dz[FT_PAW];
+#pragma unroll
+                    for (int k = 0; k < FT_PAW; ++k) {
+                        a[k] = t + k < na;
+                        jj[k] = a[k] ? (int)S.lst[lrow + t + k] : s_i;
                     }
-                    const AccT qx0 = acc_q(dx0, s0), qy0 = acc_q(dy0, s0), qz0 = acc_q(dz0, s0);
-                    const AccT qx1 = acc_q(dx1, s1), qy1 = acc_q(dy1, s1), qz1 = acc_q(dz1, s1);
-                    ax += qx0 + qx1;
-                    ay += qy0 + qy1;
-                    az += qz0 + qz1;
-                    if (a0) acc_add(S, frc, j0, -qx0, -qy0, -qz0);
-                    if (a1) acc_add(S, frc, j1, -qx1, -qy1, -qz1);
+#pragma unroll
+                    for (int k = 0; k < FT_PAW; ++k) vv[k] = S.sv[jj[k]];
+#pragma unroll
+                    for (int k = 0; k < FT_PAW; ++k)
+                        sv[k] = pair_core<KMODE>(pp, px, py, pz, vi, S.sx[jj[k]], S.sy[jj[k]], S.sz[jj[k]], vv[k], ks,
+                                                 dx[k], dy[k], dz[k], amax);
+                    if constexpr (RECORD) {
+#pragma unroll
+                        for (int k = 0; k < FT_PAW; ++k)
+                            if (a[k]) pair_record<KMODE>(vi, vv[k], dx[k], dy[k], dz[k], ks, rec);
+                    }
+#pragma unroll
+                    for (int k = 0; k < FT_PAW; ++k) {
+                        const AccT qx = acc_q(dx[k], sv[k]), qy = acc_q(dy[k], sv[k]), qz = acc_q(dz[k], sv[k]);
+                        ax += qx;
+                        ay += qy;
+                        az += qz;
+                        if (a[k]) acc_add(S, frc, jj[k], -qx, -qy, -qz);
+                    }
                 }
 #else
 #pragma unroll kFtPaUnroll
