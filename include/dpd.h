@@ -180,7 +180,11 @@ int dpd_set_particles_typed(dpd_ctx *ctx, int64_t n, const float *pos, const flo
  *   F = F(x, u, s);  v = u + dt/2 (F + f_body)
  * implemented fused (kick-drift on the half-step velocity u).
  * Synchronises the context's stream before returning and reports the first device-side
- * error (DPD_ERR_NUMERIC / DPD_ERR_CAPACITY / DPD_ERR_COMM). */
+ * error (DPD_ERR_NUMERIC / DPD_ERR_CAPACITY / DPD_ERR_COMM).  DPD_ERR_NUMERIC also covers a
+ * single pair force too large for the tiled kernel's fixed-point sums: |F_ij| above
+ * a + 6.7 sigma/sqrt(dt) + 20 gamma max(1, sqrt(kT)) rounded up to a power of two (a pair
+ * approaching at > ~20 sqrt(kT)), i.e. a diverged state; the step's results are then not
+ * to be used (the reference kernel, option "force_kernel" 1, has no such bound). */
 int dpd_step(dpd_ctx *ctx, int64_t nsteps);
 
 /* As dpd_step but does not synchronise; a device-side error is reported by the next
