@@ -70,9 +70,6 @@ constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32
 #ifndef FT_PA2
 #define FT_PA2 1
 #endif
-#ifndef FT_SW2
-#define FT_SW2 0 // two candidate quads per sweep iteration
-#endif
 #ifndef FT_PAW
 #define FT_PAW 2 // phase-A entries per iteration (FT_PA2)
 #endif
@@ -737,30 +734,6 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
             q2 = q3;
             q3 = q4;
             q4 = 0;
-#if FT_SW2
-            // two candidate quads per iteration: the loop control and the segment pop are paid
-            // once per 8 candidates; the second quad is masked when it starts at or past the
-            // segment end (then its address repeats the first quad's: no read past the rows)
-            while (j < hi) {
-                if ((int)(lptr - lbase) > 2 * (FT_LCAP - 8)) { // list full (~4 sigma): the rest in place
-                    full = true;
-                    break;
-                }
-                const bool v2 = j + 4 < hi;
-                float ra, rb, rc, rd, re, rf, rg, rh;
-                r2_quad(S, j, PX, PY, PZ, ra, rb, rc, rd);
-                r2_quad(S, v2 ? j + 4 : j, PX, PY, PZ, re, rf, rg, rh);
-                const float rc2b = v2 ? pp.rc2 : -1.0f;
-                append_if(lptr, ra, pp.rc2, (unsigned)j);
-                append_if(lptr, rb, pp.rc2, (unsigned)(j + 1));
-                append_if(lptr, rc, pp.rc2, (unsigned)(j + 2));
-                append_if(lptr, rd, pp.rc2, (unsigned)(j + 3));
-                append_if(lptr, re, rc2b, (unsigned)(j + 4));
-                append_if(lptr, rf, rc2b, (unsigned)(j + 5));
-                append_if(lptr, rg, rc2b, (unsigned)(j + 6));
-                append_if(lptr, rh, rc2b, (unsigned)(j + 7));
-                j += 8;
-#else
 #pragma unroll kFtSwUnroll
             while (j < hi) {
                 if ((int)(lptr - lbase) > 2 * (FT_LCAP - 4)) { // list full (~4 sigma): the rest in place
@@ -774,7 +747,6 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 append_if(lptr, rc, pp.rc2, (unsigned)(j + 2));
                 append_if(lptr, rd, pp.rc2, (unsigned)(j + 3));
                 j += 4;
-#endif
                 if (j >= hi) { // next segment (predicated pop)
                     j = (int)(q0 & 0xFFFFu);
                     hi = (int)(q0 >> 16);
