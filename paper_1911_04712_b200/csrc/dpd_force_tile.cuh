@@ -966,7 +966,8 @@ __global__ void __launch_bounds__(FT_NTHR, FT_MINB)
     // next step's force pass) is zeroed here, a slice per CTA: this kernel leaves HBM idle, so
     // k_scatter no longer writes a zeroed force array
 #ifndef FZERO_CTAS
-#define FZERO_CTAS 444 // the first wave (3 tiles x 148 SMs): the zeroed lines age out of L2 before k_bin
+#define FZERO_CTAS 888 // the first two waves (2 x 3 tiles x 148 SMs): the zeroed lines age out of L2 before
+                        // k_bin (v65: 296 / 444 / 888 / all CTAs: 0.4309 / 0.4309 / 0.4297 / 0.4327 ms per step)
 #endif
     if (fzero) {
         const int nb = min((int)(gridDim.x * gridDim.y * gridDim.z), FZERO_CTAS);
