@@ -73,9 +73,6 @@ constexpr int FT_WSTRIDE = 34;                // per-warp owner-table stride (32
 #ifndef FT_PAW
 #define FT_PAW 2 // phase-A entries per iteration (FT_PA2)
 #endif
-#ifndef FT_PB2
-#define FT_PB2 0 // phase B: a second entry of the same owner per iteration
-#endif
 constexpr int kFtPaUnroll = FT_PA_UNROLL;     // unroll of the phase-A pair loop (1: none)
 constexpr int kFtSwUnroll = FT_SW_UNROLL;     // unroll of the sweep loop (1: none)
 
@@ -891,35 +888,6 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
 #pragma unroll
             for (int k = 0; k < FT_NCUR; ++k) cursor_init(cu[k], S, min(t0 + k * q, t1), min(t0 + (k + 1) * q, t1), wb, nown);
             float amax = 0.0f;
-#if FT_PB2
-            // one cursor; a second entry of the SAME owner rides along when the chunk and the
-            // owner's list both extend past t (two Philox / Box-Muller chains, no second owner)
-            static_assert(FT_NCUR == 1, "FT_PB2 pairs entries of one cursor");
-            PairCursor &c0 = cu[0];
-            while (c0.t < c0.t1) {
-                const int j0 = cursor_next(c0, S, frc); // switches owner first when t crosses it
-                const bool has2 = c0.t + 1 < c0.t1 && c0.t + 1 < c0.enext;
-                const int j1 = has2 ? (int)S.lst[c0.lrow + c0.t + 1] : c0.si; // idle: self pair
-                const float4 v0 = S.sv[j0], v1 = S.sv[j1];
-                float dx0, dy0, dz0, dx1, dy1, dz1;
-                const float s0 = pair_core<KMODE>(pp, c0.px, c0.py, c0.pz, c0.vi, S.sx[j0], S.sy[j0], S.sz[j0], v0, ks,
-                                                  dx0, dy0, dz0, amax);
-                const float s1 = pair_core<KMODE>(pp, c0.px, c0.py, c0.pz, c0.vi, S.sx[j1], S.sy[j1], S.sz[j1], v1, ks,
-                                                  dx1, dy1, dz1, amax);
-                if constexpr (RECORD) {
-                    pair_record<KMODE>(c0.vi, v0, dx0, dy0, dz0, ks, rec);
-                    if (has2) pair_record<KMODE>(c0.vi, v1, dx1, dy1, dz1, ks, rec);
-                }
-                const AccT qx0 = acc_q(dx0, s0), qy0 = acc_q(dy0, s0), qz0 = acc_q(dz0, s0);
-                const AccT qx1 = acc_q(dx1, s1), qy1 = acc_q(dy1, s1), qz1 = acc_q(dz1, s1);
-                c0.fx += qx0 + qx1;
-                c0.fy += qy0 + qy1;
-                c0.fz += qz0 + qz1;
-                acc_add(S, frc, j0, -qx0, -qy0, -qz0);
-                if (has2) acc_add(S, frc, j1, -qx1, -qy1, -qz1);
-                c0.t += has2 ? 2 : 1;
-            }
-#else
             while (cu[0].t < cu[0].t1) { // later cursors are never longer than the first
                 int j[FT_NCUR];
                 bool act[FT_NCUR];
@@ -945,7 +913,6 @@ __device__ __forceinline__ void tile_pairs(ForceTileSmem &S, const TileTab &T, c
                 for (int k = 0; k < FT_NCUR; ++k)
                     cursor_accumulate(cu[k], S, frc, j[k], sv_[k], dx[k], dy[k], dz[k]); // idle: adds zeros
             }
-#endif
 #pragma unroll
             for (int k = 0; k < FT_NCUR; ++k) cursor_flush(cu[k], S, frc);
             if (amax > fx.mag_lim * fx.scale) // one pair must stay below 2^21 fixed-point units
