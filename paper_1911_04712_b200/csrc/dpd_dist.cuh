@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps pe
                        float mag_lim, uint32_t s_lo, uint32_t s_hi, int *err)
 {
     __shared__ unsigned qbuf[kHcWarps][32 + 32 * kHcI]; // < 32 pending + kHcI x 32 new
-    __shared__ float4 spi[kHcWarps][32];                // the cell's local positions (broadcast reads)
+    __shared__ float4 spi[kHcWarps][32 + kHcI];         // the cell's local positions (broadcast reads);
+                                                        // slots >= ni hold a far-away point
     __shared__ float4 svi[kHcWarps][32];                // ... and velocities
     __shared__ float4 sgp[kHcWarps][kHcG];              // staged ghosts: local-frame position, id bits
     __shared__ float4 sgv[kHcWarps][kHcG];              // ... velocity, species
@@ -334,7 +335,10 @@ __global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps pe
                 vi = vel[s0 + ib + lane];
             }
             acc[warp][0][lane] = acc[warp][1][lane] = acc[warp][2][lane] = 0;
-            spi[warp][lane] = pi;
+            // slots past the cell's particles (and the kHcI overhang of the last round) are
+            // far away: they fail r^2 < r_c^2, so the candidate test needs no index predicate
+            spi[warp][lane] = lane < ni ? pi : make_float4(1.0e18f, 1.0e18f, 1.0e18f, 0.0f);
+            if (lane < kHcI) spi[warp][32 + lane] = make_float4(1.0e18f, 1.0e18f, 1.0e18f, 0.0f);
             svi[warp][lane] = vi;
             for (int gb = 0; gb < G; gb += kHcG) {
                 const int gn = min(kHcG, G - gb);
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps pe
                         const float r2 = rx * rx + ry * ry + rz * rz;
                         const float dv = rx * (u.x - vj.x) + ry * (u.y - vj.y) + rz * (u.z - vj.z);
                         float mag;
-                        const float sc = pair_mag<KMODE>(pp, r2, dv, (uint32_t)__float_as_int(p.w),
+                        const float sc = pair_mag<KMODE>(pp, fmaxf(r2, 1e-30f), dv, (uint32_t)__float_as_int(p.w),
                                                          (uint32_t)__float_as_int(pj.w), ks, __float_as_int(u.w),
                                                          __float_as_int(vj.w), mag);
                         amax = fmaxf(amax, fabsf(mag));
@@ -397,10 +401,12 @@ __global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps pe
                         bool h[kHcI];
 #pragma unroll
                         for (int u = 0; u < kHcI; ++u) {
-                            const float4 p = spi[warp][min(ii + u, 31)]; // LDS.128 broadcast
+                            const float4 p = spi[warp][ii + u]; // LDS.128 broadcast
                             const float rx = p.x - px, ry = p.y - py, rz = p.z - pz;
                             const float r2 = rx * rx + ry * ry + rz * rz;
-                            h[u] = ii + u < ni && r2 < pp.rc2 && r2 > 0.0f;
+                            // one predicate: padded slots are far away, and a coincident pair
+                            // (r^2 = 0) evaluates to zero force (clamped r^2, d = 0; C-11)
+                            h[u] = r2 < pp.rc2;
                             m[u] = __ballot_sync(0xffffffffu, h[u]);
                         }
                         const unsigned lt = lanemask_lt();
