@@ -50,7 +50,10 @@ constexpr int FT_GAP = 3;                     // far-away sentinel slots after e
 constexpr int FT_ROWPAD = 1;                  // one extra table entry per staged row: the row's end
 constexpr int FT_SCAP = 1088;                 // staged particles + 18 row gaps (mean 864 + 54, sd 29)
 constexpr int FT_HCAP = 352;                  // home particles (mean 256, sd 16)
-constexpr int FT_LCAP = 40;                   // hits per home particle (mean 16.8, sd 4.1)
+#ifndef FT_LCAP_DEF
+#define FT_LCAP_DEF 40
+#endif
+constexpr int FT_LCAP = FT_LCAP_DEF;                 // hits per home particle (mean 16.8, sd 4.1)
 constexpr int FT_LSTRIDE = FT_LCAP + 2;       // 21 words per list (odd): conflict-free appends
 #ifndef FT_NCUR_DEF
 #define FT_NCUR_DEF 1
