@@ -162,7 +162,7 @@ struct dpd_ctx {
     double cap_factor = 1.0;
     bool msgs_ready = false;
     DevBuf<int> rank_in, gcount, gstart, grank;
-    DevBuf<int> blist; // [0]: count, then the local indices of the boundary-layer particles (row a9)
+    DevBuf<int> blist; // [0]: count, then the packed coordinates of the non-empty boundary cells (row a9)
     DevBuf<float4> gpos, gvel;
     DevBuf<unsigned long long> gscan_state;
     int64_t gcap = 0;
@@ -1133,6 +1133,8 @@ int setup_geometry(dpd_ctx *c, const double len[3], const int split[3])
     for (int k = 0; k < 3; ++k) {
         const int nd = (int)std::floor(len[k] / c->rc);
         if (nd < 3) return fail(c, DPD_ERR_CONFIG, "subdomain needs >= 3 cells per dimension (dim %d: %d)", k, nd);
+        if ((split[0] || split[1] || split[2]) && nd >= 1024) // boundary-cell list: 10-bit coordinates
+            return fail(c, DPD_ERR_CONFIG, "a decomposed subdomain needs < 1024 cells per dimension (dim %d: %d)", k, nd);
         g.n[k] = nd;
         g.split[k] = split[k];
         g.off[k] = split[k] ? 1 : 0;

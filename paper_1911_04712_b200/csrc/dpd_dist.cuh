@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) k_ghost_scatter(Msgs rec, Geom g, int max
 // direction its position calls for (face / edge / corner: a corner cell's particles go to 7
 // messages), shifted by -D L_sub into the receiver's frame, with one warp-aggregated slot
 // reservation per direction; the cell itself is appended to the boundary-cell list
-// blist[1..blist[0]] that drives the halo force (row a9).  The order inside a message is
+// blist[1..blist[0]] (packed interior coordinates) that drives the halo force (row a9).  The order inside a message is
 // irrelevant: the receiver bins the ghosts into its halo ring.
 constexpr int kGpThreads = 128; // x-extent of a block; grid (ceil(n_x / 128), n_y, n_z)
 
@@ -196,7 +196,10 @@ __global__ void __launch_bounds__(kGpThreads) k_ghost_pack_cells(const float4 *_
             int base = 0;
             if (lane == 0) base = atomicAdd(&blist[0], __popc(bm));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (has) blist[1 + base + __popc(bm & lanemask_lt())] = gc;
+            // packed interior coordinates (10 bits each; setup_geometry keeps n < 1024 in
+            // decomposed contexts): the halo kernel needs them and the extended index, and
+            // rebuilding the index is cheaper than dividing it back into coordinates
+            if (has) blist[1 + base + __popc(bm & lanemask_lt())] = ic[0] | (ic[1] << 10) | (ic[2] << 20);
         }
     }
     // ghost messages, one direction at a time over the directions any lane needs
@@ -304,9 +307,9 @@ __global__ void __launch_bounds__(32 * kHcWarps, 9) // 56 registers: 36 warps pe
     const int nbc = bcells[0];
     float amax = 0.0f; // largest pair force magnitude: the fixed-point range check
     for (int w = blockIdx.x * kHcWarps + warp; w < nbc; w += gridDim.x * kHcWarps) {
-        const int gc = bcells[1 + w];
-        const int ci[3] = {gc % g.ext[0] - g.off[0], (gc / g.ext[0]) % g.ext[1] - g.off[1],
-                           gc / (g.ext[0] * g.ext[1]) - g.off[2]};
+        const int pc = bcells[1 + w]; // packed interior coordinates (k_ghost_pack_cells)
+        const int ci[3] = {pc & 1023, (pc >> 10) & 1023, pc >> 20};
+        const int gc = (ci[0] + g.off[0]) + g.ext[0] * ((ci[1] + g.off[1]) + g.ext[1] * (ci[2] + g.off[2]));
         const int s0 = start[gc], ntot = start[gc + 1] - s0;
         // halo neighbour d of this cell on lane d: ghost range and periodic shift
         int ha = 0, hn = 0;
