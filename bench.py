@@ -460,10 +460,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = capi.dpd_get_launch_count(ctx)
     barrier()
+    # all K steps are enqueued before the NVML sampler starts: its driver queries then run
+    # while the GPU drains the queued steps (still inside the timed region) and cannot delay
+    # a kernel launch (an NVML call contending with the launches cost up to ~3 % in a run)
+    ev0.record(stream)
+    capi.dpd_step_async(ctx, args.steps)
+    ev1.record(stream)
     with ClockSampler(local_rank) as clocks:
-        ev0.record(stream)
-        capi.dpd_step_async(ctx, args.steps)
-        ev1.record(stream)
         capi.dpd_sync(ctx)
     barrier()
     launches = capi.dpd_get_launch_count(ctx) - l0
