@@ -458,12 +458,37 @@ int phase_ghost_pack(dpd_ctx *c, cudaStream_t st = nullptr)
     CUDA_TRY(c, c->blist.reserve((size_t)g.ncell + 1));
     CUDA_TRY(c, cudaMemsetAsync(c->blist.p, 0, sizeof(int), st));
     TRY(launch(c, KID_GHOST_PACK, [&] { k_zero_headers<<<1, 32, 0, st>>>(gs); }, st));
-    const dim3 grid((g.n[0] + kGpThreads - 1) / kGpThreads, g.n[1], g.n[2]);
+    // the boundary cells as disjoint boxes, one per split dimension (GpPlan in dpd_dist.cuh)
+    GpPlan pl{};
+    int total = 0;
+    for (int k = 0; k < 3; ++k) {
+        if (!g.split[k]) continue;
+        const int x = pl.nbox++;
+        pl.dimk[x] = k;
+        int cells = 1;
+        for (int d = 0; d < 3; ++d) {
+            if (d == k) {
+                pl.lo[x][d] = 0;
+                pl.ext[x][d] = 2; // {0, n - 1}
+            } else if (g.split[d] && d < k) {
+                pl.lo[x][d] = 1;
+                pl.ext[x][d] = g.n[d] - 2; // inner range: its faces belong to box d
+            } else {
+                pl.lo[x][d] = 0;
+                pl.ext[x][d] = g.n[d];
+            }
+            cells *= pl.ext[x][d];
+        }
+        total += cells;
+        pl.end[x] = total;
+    }
+    if (pl.nbox == 0 || total == 0) return DPD_OK;
+    const unsigned grid = (unsigned)(((int64_t)total * kGpSub + kGpThreads - 1) / kGpThreads);
     return launch(
         c, KID_GHOST_PACK,
         [&] {
             k_ghost_pack_cells<<<grid, kGpThreads, 0, st>>>(c->pos[c->cur].p, c->vel[c->cur].p, c->start[c->scur].p, g,
-                                                            gs, c->blist.p, c->err.p);
+                                                            gs, c->blist.p, c->err.p, pl);
         },
         st);
 }

@@ -155,15 +155,50 @@ __global__ void __launch_bounds__(256) k_ghost_scatter(Msgs rec, Geom g, int max
 // reservation per direction; the cell itself is appended to the boundary-cell list
 // blist[1..blist[0]] (packed interior coordinates) that drives the halo force (row a9).  The order inside a message is
 // irrelevant: the receiver bins the ghosts into its halo ring.
-constexpr int kGpThreads = 128; // x-extent of a block; grid (ceil(n_x / 128), n_y, n_z)
+constexpr int kGpThreads = 128; // 1D grid over the boundary cells (GpPlan)
+#ifndef GP_SUB
+#define GP_SUB 1
+#endif
+constexpr int kGpSub = GP_SUB;  // threads per boundary cell (a power of two <= 32); 2x2x2 group
+                                // overhead at 128^3 per subdomain: 1 -> 6.9 %, 4 -> 7.5 %, 8 -> 8.7 %
+
+// The boundary cells of a subdomain (a split dimension's first or last interior layer) as
+// disjoint boxes, one per split dimension k: coordinate k on {0, n_k - 1}, the split
+// dimensions before k restricted to their inner range [1, n - 2], the others full.  A
+// thread's linear index b walks the boxes in order, x fastest, so every lane of a warp has a
+// boundary cell (the round-1/2 kernel ran one thread per interior cell and left ~half of
+// the lanes of the x-face warps idle).
+struct GpPlan {
+    int nbox;        // number of boxes (split dimensions)
+    int end[3];      // exclusive prefix end of each box's cell count
+    int lo[3][3];    // per box: lower coordinate per dimension
+    int ext[3][3];   // per box: extent per dimension (dimension k of box k: 2, stride n_k - 1)
+    int dimk[3];     // per box: its split dimension
+};
 
 __global__ void __launch_bounds__(kGpThreads) k_ghost_pack_cells(const float4 *__restrict__ pos,
                                                                  const float4 *__restrict__ vel,
                                                                  const int *__restrict__ start, Geom g, Msgs gs,
-                                                                 int *__restrict__ blist, int *err)
+                                                                 int *__restrict__ blist, int *err, GpPlan pl)
 {
     const int lane = threadIdx.x & 31;
-    const int ic[3] = {(int)(blockIdx.x * kGpThreads + threadIdx.x), (int)blockIdx.y, (int)blockIdx.z};
+    // kGpSub consecutive lanes share a boundary cell and split its copies (more loads in
+    // flight per cell); the cell's lane 0 (sub == 0) does the list entry and reservations
+    const int sub = lane & (kGpSub - 1);
+    const int b = (blockIdx.x * kGpThreads + threadIdx.x) / kGpSub;
+    int ic[3] = {g.n[0], 0, 0}; // past the grid: no work
+    if (b < pl.end[pl.nbox - 1]) {
+        int x = 0;
+        while (x + 1 < pl.nbox && b >= pl.end[x]) ++x;
+        int r = b - (x > 0 ? pl.end[x - 1] : 0);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int e = pl.ext[x][k];
+            const int v = r % e;
+            r /= e;
+            ic[k] = pl.lo[x][k] + (k == pl.dimk[x] ? v * (g.n[k] - 1) : v);
+        }
+    }
     unsigned dmask = 0;
     int s0 = 0, cnt = 0, gc = 0;
     bool border = false;
@@ -190,7 +225,7 @@ __global__ void __launch_bounds__(kGpThreads) k_ghost_pack_cells(const float4 *_
     }
     // boundary-cell list (extended-grid index of every non-empty boundary cell)
     {
-        const bool has = border && cnt > 0;
+        const bool has = border && cnt > 0 && sub == 0;
         const unsigned bm = __ballot_sync(0xffffffffu, has);
         if (bm) {
             int base = 0;
@@ -208,7 +243,8 @@ __global__ void __launch_bounds__(kGpThreads) k_ghost_pack_cells(const float4 *_
         const int d = __ffs(wm) - 1;
         wm &= wm - 1;
         const int v = ((dmask >> d) & 1u) ? cnt : 0;
-        int incl = v;
+        const int vs = sub == 0 ? v : 0; // each cell counted once
+        int incl = vs;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -218,20 +254,20 @@ __global__ void __launch_bounds__(kGpThreads) k_ghost_pack_cells(const float4 *_
         int base = 0;
         if (lane == 31) base = atomicAdd(msg_count(gs, d), tot);
         base = __shfl_sync(0xffffffffu, base, 31);
+        const int slot0 = __shfl_sync(0xffffffffu, base + incl - vs, lane & ~(kGpSub - 1));
         if (v) {
             const int dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
             const float shx = dx * g.L[0], shy = dy * g.L[1], shz = dz * g.L[2];
             float4 *q = msg_data(gs, d);
-            const int slot0 = base + incl - v;
             const int vfit = max(0, min(v, gs.cap[d] - slot0)); // overflow: counted, not written
             // no branch in the copy loop: the loads of several particles are in flight
-#pragma unroll 4
-            for (int k = 0; k < vfit; ++k) {
+#pragma unroll 2
+            for (int k = sub; k < vfit; k += kGpSub) {
                 const float4 p = pos[s0 + k], u = vel[s0 + k];
                 q[2 * (slot0 + k)] = make_float4(p.x - shx, p.y - shy, p.z - shz, p.w);
                 q[2 * (slot0 + k) + 1] = u;
             }
-            if (vfit < v) raise_err(err, ERR_CAPACITY, __float_as_int(pos[s0 + vfit].w));
+            if (vfit < v && sub == 0) raise_err(err, ERR_CAPACITY, __float_as_int(pos[s0 + vfit].w));
         }
     }
 }
