@@ -316,7 +316,11 @@ __device__ __forceinline__ int halo_cell(const Geom &g, const int ci[3], int d, 
 // with both sides read from shared memory.  One-sided (C-19): the i-side sums go to
 // fixed-point shared accumulators, then once to frc.
 constexpr int kHcWarps = 4;
-constexpr int kHcI = 4;   // local particles tested per candidate round
+#ifndef HC_I
+#define HC_I 4
+#endif
+constexpr int kHcI = HC_I;   // local particles tested per candidate round (2 / 4 / 8: halo 184 / 177 / 200 us
+                             // per 128^3 loopback step)
 #ifndef KHC_G
 #define KHC_G 128
 #endif
