@@ -100,3 +100,16 @@ def test_loopback_matches_single_domain(split):
             assert np.abs(a[2] - b[2]).max() < 10 * FORCE_TOL * np.abs(b[2]).max()
     finally:
         capi.dpd_destroy(c)
+
+
+def test_loopback_rejects_too_many_cells_per_dimension():
+    """The boundary-cell list packs 10-bit cell coordinates: a decomposed subdomain must stay
+    below 1024 cells per dimension, refused at create (DPD_ERR_CONFIG), not overflowed."""
+    from paper_1911_04712_b200 import capi
+    cfg = workloads.CONFIGS["parity"]
+    with pytest.raises(capi.DPDError):
+        capi.dpd_create_loopback((1100.0, 4.0, 4.0), cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed,
+                                 (0, 1, 0))
+    c = capi.dpd_create_loopback((1000.0, 4.0, 4.0), cfg.rc, cfg.a, cfg.gamma, cfg.kT, cfg.power, cfg.dt, cfg.seed,
+                                 (0, 1, 0))
+    capi.dpd_destroy(c)
